@@ -1,0 +1,386 @@
+"""Benchmark of the fused DG volume kernel (BASELINE.json metric: GDOF/s and
+achieved HBM GB/s, Nq=8 fp64 volume kernel, 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one launch of the fused volume kernel over all of this rank's
+elements (rhsq += v). Workload: BASELINE config 2, Nq=8, Ne=32768 fp64 per
+GPU (weak scaling: N GPUs hold N*32768 elements; N=8 is config 3,
+Ne=262144). Inputs are the reference's ``make_inputs`` distributions
+(seed 1 + rank), upcast to fp64 — synthetic data. The working set (4.56 GB
+per GPU) is ~36x the 126 MB L2, so no L2 flush is needed between steps.
+
+Rank 0 prints one JSON line. See DESIGN.md §Measurement for the fields.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GDOF/s, Nq=8 fp64 volume kernel (grid points per second)"
+UNIT = "GDOF/s"
+
+
+def bytes_per_point(dtype_bytes: int) -> int:
+    # q 8 + g 9 + Jinv 1 read, rhsq 8 read + 8 written
+    return 34 * dtype_bytes
+
+
+def flops_per_point(nq: int) -> int:
+    # 168 + 48*Nq with FMA = 2 flops
+    return 168 + 48 * nq
+
+
+def measured_peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        doc = json.loads(p.read_text())
+        return float(doc["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel_key)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# --------------------------------------------------------------------------
+# CPU reference path (the oracle port of lf/bench/reference.py:36-69)
+# --------------------------------------------------------------------------
+
+_POOL_STATE = None
+
+
+def _pool_work(rng):
+    from oracle import volterm as O
+    a, b = rng
+    O.volume_term_f64(_POOL_STATE, elements=range(a, b))
+    return b - a
+
+
+def cpu_reference_time(state, n_elements: int, cores: int, pool=None):
+    """Wall time of the reference's per-element numpy algorithm over the
+    first ``n_elements`` elements, sharded over ``cores`` processes."""
+    global _POOL_STATE
+    _POOL_STATE = state
+    chunks = [(n_elements * i // cores, n_elements * (i + 1) // cores)
+              for i in range(cores)]
+    chunks = [c for c in chunks if c[1] > c[0]]
+    t0 = time.perf_counter()
+    if pool is None:
+        for c in chunks:
+            _pool_work(c)
+    else:
+        pool.map(_pool_work, chunks, chunksize=1)
+    return time.perf_counter() - t0
+
+
+def make_pool(cores: int, state):
+    """Fork the worker pool AFTER publishing ``state`` (copy-on-write)."""
+    global _POOL_STATE
+    import multiprocessing as mp
+    _POOL_STATE = state
+    if cores <= 1:
+        return None
+    return mp.get_context("fork").Pool(cores)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run_reference(args) -> None:
+    """--impl reference: the reference's CPU path (oracle port, all host
+    cores) on the same workload config, bounded samples per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1604_08501_b200 import BenchmarkConfig, make_inputs
+    cores = host_cores()
+    # ~2.2 ms per element per core at Nq=8; keep the whole
+    # run near 2 minutes of wall time whatever K and W are
+    per_elem = 2.2e-3 * (args.nq / 8) ** 3 if args.nq > 8 else 2.2e-3
+    budget_s = 120.0
+    per_step = int(budget_s / max(1, args.steps + args.warmup) / per_elem) * cores
+    per_step = max(cores, min(per_step, 64 * cores, args.ne))
+    state = make_inputs(BenchmarkConfig(nq=args.nq, ne=per_step, seed=1))
+    pool = make_pool(cores, state)
+    try:
+        for _ in range(args.warmup):
+            cpu_reference_time(state, per_step, cores, pool)
+        t = 0.0
+        for _ in range(args.steps):
+            t += cpu_reference_time(state, per_step, cores, pool)
+    finally:
+        if pool is not None:
+            pool.close()
+            pool.join()
+    pts = args.nq ** 3 * per_step
+    value = pts * args.steps / t / 1e9
+    sample = (f"{per_step} elements (Nq={args.nq}) per step, reference "
+              f"per-element numpy algorithm (oracle/volterm.py port of "
+              f"lf/bench/reference.py:36-69), fp64, {cores} processes")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (make_inputs distributions, seed 1)",
+        "config": {"workload": f"Nq={args.nq} volume term, sample of "
+                               f"{per_step} elements per step",
+                   "nq": args.nq, "ne_per_gpu": args.ne},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU path
+# --------------------------------------------------------------------------
+
+def e2e_run(ds, host, steps: int, warmup: int, chunks: int, variant: str):
+    """End to end through the public API with pinned HOST buffers: every
+    step copies q, g, Jinv, rhsq host->device, runs the kernel and reads
+    rhsq back, chunked over elements on two streams so copies overlap the
+    kernel. Returns (seconds per step, h2d bytes, d2h bytes, launches)."""
+    import torch
+    from paper_1604_08501_b200 import volume_rhs_device
+    from paper_1604_08501_b200.distributed import shard_range
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ne = ds.ne
+    ranges = [shard_range(ne, c, chunks) for c in range(chunks)]
+    launches = 0
+
+    def one_step():
+        nonlocal launches
+        for c, (a, b) in enumerate(ranges):
+            s = streams[c % 2]
+            with torch.cuda.stream(s):
+                for name in ("q", "g", "Jinv", "rhsq"):
+                    getattr(ds, name)[a:b].copy_(host[name][a:b], non_blocking=True)
+                volume_rhs_device(ds.shard(a, b), variant=variant, stream=s)
+                launches += 1
+                host["out"][a:b].copy_(ds.rhsq[a:b], non_blocking=True)
+        for s in streams:
+            s.synchronize()
+
+    for _ in range(warmup):
+        one_step()
+    torch.cuda.synchronize()
+    launches = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    h2d = sum(host[n].numel() * host[n].element_size() for n in ("q", "g", "Jinv", "rhsq"))
+    d2h = host["out"].numel() * host["out"].element_size()
+    return dt, h2d, d2h, launches
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_08501_b200 import (BenchmarkConfig, DeviceFieldState,
+                                       make_inputs, volume_rhs_device)
+    from paper_1604_08501_b200 import _native
+    from paper_1604_08501_b200.distributed import global_checksum, max_over_ranks
+    from paper_1604_08501_b200.telemetry import ClockSampler
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    nbytes = 8 if dt == torch.float64 else 4
+    nq, ne = args.nq, args.ne
+    state = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=1 + rank))
+    ds = DeviceFieldState.from_field_state(state, dtype=dt, device=dev)
+    variant = args.variant
+    resolved = _native.resolve_variant(nbytes, nq) if variant == "auto" else variant
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        volume_rhs_device(ds, variant=variant, stream=stream)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            volume_rhs_device(ds, variant=variant, stream=stream)
+            ends[k].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    total_ms = max_over_ranks(total_ms, device=dev)
+    launch_ms_max = max_over_ranks(launch_ms, device=dev)
+    ms_per_step = total_ms / args.steps
+
+    pts_rank = nq ** 3 * ne
+    pts_total = pts_rank * world
+    value = pts_total / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    alg_bytes = bytes_per_point(nbytes) * pts_rank
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+    kernel_key = f"{resolved}|nq={nq}|{args.dtype}"
+    traffic = ncu_traffic(kernel_key)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_point": bytes_per_point(nbytes),
+                "launch_ms": launch_ms, "launch_ms_max_over_ranks": launch_ms_max,
+                "frac_of_8tbs_nominal": achieved / 8000.0,
+                "flops_per_point": flops_per_point(nq),
+                "achieved_tflops": flops_per_point(nq) * pts_rank / (launch_ms * 1e-3) / 1e12,
+                "kernel": kernel_key}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = {n: getattr(ds, n).cpu().pin_memory() for n in ("q", "g", "Jinv", "rhsq")}
+        host["out"] = torch.empty_like(host["rhsq"]).pin_memory()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        with ClockSampler(local) as e2e_clocks:
+            sec, h2d, d2h, e2e_launches = e2e_run(ds, host, e2e_steps, 1,
+                                                  args.e2e_chunks, variant)
+        sec = max_over_ranks(sec, device=dev)
+        e2e = {"value": pts_total / sec / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": sec * 1e3, "steps": e2e_steps,
+               "chunks": args.e2e_chunks, "launches": e2e_launches,
+               "api": "DeviceFieldState + volume_rhs_device over pinned host "
+                      "buffers (element-batched layout), 2 streams",
+               "clocks": e2e_clocks.summary()}
+        del host
+
+    checksum = global_checksum(ds.rhsq).tolist()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = host_cores()
+        n = min(ne, max(cores, args.cpu_sample_per_core * cores))
+        pool = make_pool(cores, state)
+        try:
+            cpu_reference_time(state, min(n, cores), cores, pool)  # warm pool
+            t = cpu_reference_time(state, n, cores, pool)
+        finally:
+            if pool is not None:
+                pool.close()
+                pool.join()
+        cpu = {"value": nq ** 3 * n / t / 1e9, "unit": UNIT, "cores": cores,
+               "kind": "port",
+               "sample": f"{n} elements of this workload (Nq={nq}), the "
+                         f"reference's per-element numpy algorithm "
+                         f"(oracle/volterm.py, port of lf/bench/reference.py:"
+                         f"36-69) in {cores} processes, {t:.2f} s wall"}
+        if not args.no_cpu_c:
+            from oracle import coracle
+            qh, gh, jh, dh = coracle.to_element_batched(
+                make_inputs(BenchmarkConfig(nq=nq, ne=min(ne, 4096), seed=1)))
+            nc = qh.shape[0]
+            coracle.volume_f64_eb(nq, qh[:cores], gh[:cores], jh[:cores], dh,
+                                  state.constants, nthreads=cores)
+            t0 = time.perf_counter()
+            coracle.volume_f64_eb(nq, qh, gh, jh, dh, state.constants,
+                                  nthreads=cores)
+            tc = time.perf_counter() - t0
+            cpu["c_port"] = {"value": nq ** 3 * nc / tc / 1e9, "cores": cores,
+                             "sample": f"{nc} elements, C restatement "
+                                       f"(oracle/volterm_oracle.c) -O2, "
+                                       f"{cores} pthreads, {tc:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": f"synthetic: reference make_inputs distributions "
+                    f"(seed 1+rank) upcast to {args.dtype}",
+            "config": {"workload": f"BASELINE config {'2' if world == 1 else '3'}: "
+                                   f"Nq={nq}, {ne} hex elements per GPU, "
+                                   f"{args.dtype}, rhsq += v",
+                       "nq": nq, "ne_per_gpu": ne, "ne_total": ne * world,
+                       "points_total": pts_total, "variant": resolved,
+                       "parallelism": f"element-sharded x{world}, no "
+                                      f"data-path collective",
+                       "l2": "working set "
+                             f"{alg_bytes / 1e9:.2f} GB/GPU >> 126 MB L2; no flush"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": args.steps,
+            "checksum": {"field_sum": checksum[:8], "field_maxabs": checksum[8:]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None) -> None:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--nq", type=int, default=8)
+    ap.add_argument("--ne", type=int, default=32768, help="elements per GPU")
+    ap.add_argument("--dtype", choices=("f64", "f32"), default="f64")
+    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-c", action="store_true")
+    ap.add_argument("--cpu-sample-per-core", type=int, default=48)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+"""ctypes binding of the C-ABI library ``_lib/liblfb_volume.so``
+(declared in ``include/lfb_volume.h``).
+
+ctypes (not a torch extension) keeps the boundary a plain C ABI: the same
+symbols a cgo / JNI / N-API binding would use. The
+library is built in-tree by ``__graft_entry__.build()``; if it is missing,
+every call raises ``NativeLibraryMissing`` — there is no fallback path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+from .diagnostics import ExecutionError, KernelLaunchError, NativeLibraryMissing
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "liblfb_volume.so"
+
+LFB_OK = 0
+LFB_ERR_BAD_NQ = 1
+LFB_ERR_BAD_NE = 2
+LFB_ERR_NULL = 3
+LFB_ERR_MISALIGNED = 4
+LFB_ERR_LAUNCH = 5
+LFB_ERR_CUDA = 6
+LFB_ERR_BAD_CONSTANTS = 7
+LFB_ERR_BAD_VARIANT = 8
+LFB_ERR_ALLOC = 9
+
+VARIANT_AUTO = 0
+VARIANT_BASIC = 1
+VARIANT_FUSED = 2
+VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED}
+
+MAX_NQ = 16
+
+#: every symbol include/lfb_volume.h declares (tests check the exports)
+EXPORTED_SYMBOLS = (
+    "lfb_volume_rhs_f64", "lfb_volume_rhs_f32",
+    "lfb_volume_rhs_variant_f64", "lfb_volume_rhs_variant_f32",
+    "lfb_variant_available", "lfb_variant_name", "lfb_resolve_variant",
+    "lfb_error_string", "lfb_version",
+)
+
+_lock = threading.Lock()
+_lib = None
+
+_i, _i64, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+_d, _f = ctypes.c_double, ctypes.c_float
+
+
+def _declare(L) -> None:
+    for name, scal in (("f64", _d), ("f32", _f)):
+        fn = getattr(L, f"lfb_volume_rhs_{name}")
+        fn.restype = _i
+        fn.argtypes = [_i, _i64, scal, scal, scal, _vp, _vp, _vp, _vp, _vp, _vp]
+        fn = getattr(L, f"lfb_volume_rhs_variant_{name}")
+        fn.restype = _i
+        fn.argtypes = [_i, _i, _i64, scal, scal, scal, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.lfb_variant_available.restype = _i
+    L.lfb_variant_available.argtypes = [_i, _i, _i]
+    L.lfb_resolve_variant.restype = _i
+    L.lfb_resolve_variant.argtypes = [_i, _i]
+    L.lfb_variant_name.restype = ctypes.c_char_p
+    L.lfb_variant_name.argtypes = [_i]
+    L.lfb_error_string.restype = ctypes.c_char_p
+    L.lfb_error_string.argtypes = [_i]
+    L.lfb_version.restype = _i
+    L.lfb_version.argtypes = []
+
+
+def lib():
+    """The loaded library (raises NativeLibraryMissing if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeLibraryMissing(
+                    f"{LIB_PATH} is not built; run __graft_entry__.build()")
+            try:
+                L = ctypes.CDLL(str(LIB_PATH))
+            except OSError as exc:  # pragma: no cover - environment specific
+                raise NativeLibraryMissing(str(exc)) from exc
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def error_string(code: int) -> str:
+    return lib().lfb_error_string(code).decode()
+
+
+def check(code: int, what: str = "lfb call") -> None:
+    """Map a C-ABI return code to the reference-style exception."""
+    if code == LFB_OK:
+        return
+    msg = f"{what}: {error_string(code)} (code {code})"
+    if code in (LFB_ERR_LAUNCH, LFB_ERR_CUDA, LFB_ERR_ALLOC):
+        raise KernelLaunchError(msg)
+    raise ExecutionError(msg)
+
+
+def variant_id(variant) -> int:
+    if isinstance(variant, str):
+        try:
+            return VARIANTS[variant]
+        except KeyError:
+            raise ExecutionError(f"unknown kernel variant {variant!r}") from None
+    return int(variant)
+
+
+def resolve_variant(dtype_bytes: int, nq: int) -> str:
+    L = lib()
+    return L.lfb_variant_name(L.lfb_resolve_variant(dtype_bytes, nq)).decode()
+
+
+def variant_available(variant, dtype_bytes: int, nq: int) -> bool:
+    return bool(lib().lfb_variant_available(variant_id(variant), dtype_bytes, nq))
+
+
+def volume_rhs_ptr(dtype_bytes: int, variant, nq: int, ne: int, p0: float,
+                   R: float, gam: float, q: int, rhsq: int, D: int, g: int,
+                   jinv: int, stream: int) -> None:
+    """Raw C-ABI call on device pointers (ints). Raises on a non-zero code."""
+    L = lib()
+    fn = L.lfb_volume_rhs_variant_f64 if dtype_bytes == 8 else L.lfb_volume_rhs_variant_f32
+    rc = fn(variant_id(variant), int(nq), int(ne), p0, R, gam, q, rhsq, D, g,
+            jinv, stream)
+    check(rc, "lfb_volume_rhs")

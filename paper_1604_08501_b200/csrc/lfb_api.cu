@@ -1,0 +1,146 @@
+// C-ABI entry points (include/lfb_volume.h): argument validation and
+// variant dispatch. No global mutable state.
+
+#include <stdint.h>
+
+#include "lfb_common.cuh"
+
+namespace lfb {
+int volume_basic_f64(int, int64_t, double, double, double, const double *,
+                     double *, const double *, const double *, const double *,
+                     cudaStream_t);
+int volume_basic_f32(int, int64_t, float, float, float, const float *, float *,
+                     const float *, const float *, const float *, cudaStream_t);
+int volume_fused_f64(int, int64_t, double, double, double, const double *,
+                     double *, const double *, const double *, const double *,
+                     cudaStream_t);
+int volume_fused_f32(int, int64_t, float, float, float, const float *, float *,
+                     const float *, const float *, const float *, cudaStream_t);
+bool fused_available(int dtype_bytes, int nq);
+}  // namespace lfb
+
+namespace {
+
+template <typename T>
+int validate(int nq, int64_t ne, T p0, T R, T gam, const T *q, const T *rhsq,
+             const T *D, const T *g, const T *jinv) {
+  if (nq < 1 || nq > LFB_MAX_NQ) return LFB_ERR_BAD_NQ;
+  if (ne < 0) return LFB_ERR_BAD_NE;
+  if (!(p0 > T(0) && R > T(0) && gam > T(1))) return LFB_ERR_BAD_CONSTANTS;
+  if (ne == 0) return LFB_OK;
+  if (!q || !rhsq || !D || !g || !jinv) return LFB_ERR_NULL;
+  const uintptr_t m = sizeof(T) - 1;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(rhsq) |
+       reinterpret_cast<uintptr_t>(D) | reinterpret_cast<uintptr_t>(g) |
+       reinterpret_cast<uintptr_t>(jinv)) & m)
+    return LFB_ERR_MISALIGNED;
+  return LFB_OK;
+}
+
+int resolve(int variant, int bytes, int nq) {
+  if (variant == LFB_VARIANT_AUTO)
+    return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED
+                                           : LFB_VARIANT_BASIC;
+  return variant;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
+                               double Rgas, double gam, const double *q,
+                               double *rhsq, const double *D, const double *g,
+                               const double *Jinv, void *stream) {
+  int rc = validate<double>(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv);
+  if (rc != LFB_OK || Ne == 0) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (resolve(variant, 8, Nq)) {
+    case LFB_VARIANT_BASIC:
+      return lfb::volume_basic_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_FUSED:
+      if (!lfb::fused_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_fused_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    default:
+      return LFB_ERR_BAD_VARIANT;
+  }
+}
+
+int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
+                               float Rgas, float gam, const float *q,
+                               float *rhsq, const float *D, const float *g,
+                               const float *Jinv, void *stream) {
+  int rc = validate<float>(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv);
+  if (rc != LFB_OK || Ne == 0) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (resolve(variant, 4, Nq)) {
+    case LFB_VARIANT_BASIC:
+      return lfb::volume_basic_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_FUSED:
+      if (!lfb::fused_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_fused_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    default:
+      return LFB_ERR_BAD_VARIANT;
+  }
+}
+
+int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,
+                       const double *q, double *rhsq, const double *D,
+                       const double *g, const double *Jinv, void *stream) {
+  return lfb_volume_rhs_variant_f64(LFB_VARIANT_AUTO, Nq, Ne, p0, Rgas, gam, q,
+                                    rhsq, D, g, Jinv, stream);
+}
+
+int lfb_volume_rhs_f32(int Nq, int64_t Ne, float p0, float Rgas, float gam,
+                       const float *q, float *rhsq, const float *D,
+                       const float *g, const float *Jinv, void *stream) {
+  return lfb_volume_rhs_variant_f32(LFB_VARIANT_AUTO, Nq, Ne, p0, Rgas, gam, q,
+                                    rhsq, D, g, Jinv, stream);
+}
+
+int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
+  if (Nq < 1 || Nq > LFB_MAX_NQ || (dtype_bytes != 4 && dtype_bytes != 8))
+    return 0;
+  switch (variant) {
+    case LFB_VARIANT_AUTO:
+    case LFB_VARIANT_BASIC:
+      return 1;
+    case LFB_VARIANT_FUSED:
+      return lfb::fused_available(dtype_bytes, Nq) ? 1 : 0;
+    default:
+      return 0;
+  }
+}
+
+int lfb_resolve_variant(int dtype_bytes, int Nq) {
+  return resolve(LFB_VARIANT_AUTO, dtype_bytes, Nq);
+}
+
+const char *lfb_variant_name(int variant) {
+  switch (variant) {
+    case LFB_VARIANT_AUTO: return "auto";
+    case LFB_VARIANT_BASIC: return "basic";
+    case LFB_VARIANT_FUSED: return "fused";
+    default: return "unknown";
+  }
+}
+
+const char *lfb_error_string(int code) {
+  switch (code) {
+    case LFB_OK: return "ok";
+    case LFB_ERR_BAD_NQ: return "Nq must be in [1, 16]";
+    case LFB_ERR_BAD_NE: return "Ne must be non-negative";
+    case LFB_ERR_NULL: return "missing array argument (NULL pointer)";
+    case LFB_ERR_MISALIGNED: return "array pointer not aligned to its element size";
+    case LFB_ERR_LAUNCH: return "kernel launch failed";
+    case LFB_ERR_CUDA: return "CUDA runtime error";
+    case LFB_ERR_BAD_CONSTANTS: return "need p0 > 0, R > 0, gamma > 1";
+    case LFB_ERR_BAD_VARIANT: return "unknown or unavailable kernel variant";
+    case LFB_ERR_ALLOC: return "staging allocation failed";
+    default: return "unknown error";
+  }
+}
+
+int lfb_version(void) { return (1 << 16) | 0; }
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+"""Host-side mirror of the reference's volume-term entry points, backed by
+the sm_100a CUDA kernel behind the C-ABI (``include/lfb_volume.h``).
+
+Reference entry points kept signature-compatible (``lf/`` =
+``pkg/src/loopforge/``):
+
+* ``reference_volume_term(state, c=None)`` — ``lf/bench/reference.py:36-70``:
+  the rhsq increment, fp64 accumulation, float32 result, rhsq untouched;
+* ``interpret_state(kernels, state, nq, ne)`` — ``lf/bench/driver.py:54-69``:
+  in place ``rhsq += v`` at float32 (the fused level-8 kernel's semantics),
+  returns ``(state.rhsq, envs)``;
+* ``max_rel_error`` — ``lf/bench/driver.py:72-91`` (the parity metric).
+
+New, B200-first entry points:
+
+* ``volume_term(state, c=None, *, dtype=float64)`` — increment at the chosen
+  precision (fp64 default);
+* ``volume_rhs_(state, c=None, *, dtype=None)`` — in-place update;
+* ``DeviceFieldState`` + ``volume_rhs_device`` — the device-resident hot
+  path: element-batched tensors in HBM, one stream-ordered C-ABI call.
+
+Every compute call goes through the CUDA library; if it is missing the call
+raises ``NativeLibraryMissing`` (no CPU fallback exists in this package).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .diagnostics import ExecutionError
+from .inputs import FieldState, PhysicalConstants
+
+_TORCH_DTYPES = {np.dtype(np.float32): torch.float32,
+                 np.dtype(np.float64): torch.float64}
+
+
+def _torch_dtype(dtype) -> torch.dtype:
+    if isinstance(dtype, torch.dtype):
+        if dtype not in (torch.float32, torch.float64):
+            raise ExecutionError(f"unsupported dtype {dtype}")
+        return dtype
+    try:
+        return _TORCH_DTYPES[np.dtype(dtype)]
+    except (KeyError, TypeError):
+        raise ExecutionError(f"unsupported dtype {dtype!r}") from None
+
+
+def _device(device) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise ExecutionError("no CUDA device available (this package has "
+                                 "no CPU path)")
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ExecutionError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def validate_state(state: FieldState, nq: int | None = None,
+                   ne: int | None = None, dtype=None) -> tuple[int, int]:
+    """Shape/dtype checks with the reference's error behaviour
+    (``lf/interp.py:51-74``: ``ExecutionError`` naming the array)."""
+    arrays = state.arrays()
+    for name in ("q", "rhsq", "D", "g", "Jinv"):
+        if arrays.get(name) is None:
+            raise ExecutionError(f"missing array argument {name!r}")
+    q = arrays["q"]
+    if q.ndim != 5 or q.shape[3] != 8:
+        raise ExecutionError(f"array 'q' has shape {q.shape}, expected "
+                             f"(Nq, Nq, Nq, 8, Ne)")
+    nq_ = int(q.shape[0]) if nq is None else int(nq)
+    ne_ = int(q.shape[4]) if ne is None else int(ne)
+    want = {"q": (nq_, nq_, nq_, 8, ne_), "rhsq": (nq_, nq_, nq_, 8, ne_),
+            "D": (nq_, nq_), "g": (nq_, nq_, nq_, 3, 3, ne_),
+            "Jinv": (nq_, nq_, nq_, ne_)}
+    for name, shape in want.items():
+        if tuple(arrays[name].shape) != shape:
+            raise ExecutionError(f"array {name!r} has shape "
+                                 f"{tuple(arrays[name].shape)}, kernel expects "
+                                 f"{shape}")
+        if dtype is not None and arrays[name].dtype != np.dtype(dtype):
+            raise ExecutionError(f"array {name!r} must be "
+                                 f"{np.dtype(dtype).name}")
+        if arrays[name].dtype not in (np.float32, np.float64):
+            raise ExecutionError(f"array {name!r} must be float32 or float64")
+    if not 1 <= nq_ <= _native.MAX_NQ:
+        raise ExecutionError(f"Nq={nq_} outside [1, {_native.MAX_NQ}]")
+    return nq_, ne_
+
+
+@dataclass
+class DeviceFieldState:
+    """A FieldState resident in HBM in the element-batched layout of the
+    C-ABI (the Fortran declarations' layout, ``volume.f90:14-18``):
+
+    q, rhsq ``(Ne, 8, Nq, Nq, Nq)`` = [e][field][k][j][i];
+    g ``(Ne, 3, 3, Nq, Nq, Nq)`` = [e][dir][a][k][j][i];
+    Jinv ``(Ne, Nq, Nq, Nq)`` = [e][k][j][i]; D ``(Nq, Nq)`` = [n][i].
+    """
+
+    q: torch.Tensor
+    rhsq: torch.Tensor
+    D: torch.Tensor
+    g: torch.Tensor
+    Jinv: torch.Tensor
+    constants: PhysicalConstants
+
+    @property
+    def nq(self) -> int:
+        return int(self.q.shape[2])
+
+    @property
+    def ne(self) -> int:
+        return int(self.q.shape[0])
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.q.dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self.q.device
+
+    @classmethod
+    def from_field_state(cls, state: FieldState, dtype=torch.float64,
+                         device=None) -> "DeviceFieldState":
+        """Upload and convert the reference's C-order arrays
+        ([i,j,k,b,e], element fastest) to the element-batched layout."""
+        validate_state(state)
+        dev = _device(device)
+        dt = _torch_dtype(dtype)
+
+        def up(a: np.ndarray, perm):
+            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+            return t.permute(*perm).to(dt).contiguous()
+
+        return cls(q=up(state.q, (4, 3, 2, 1, 0)),
+                   rhsq=up(state.rhsq, (4, 3, 2, 1, 0)),
+                   D=up(state.D, (1, 0)),
+                   g=up(state.g, (5, 4, 3, 2, 1, 0)),
+                   Jinv=up(state.Jinv, (3, 2, 1, 0)),
+                   constants=state.constants)
+
+    @classmethod
+    def empty(cls, nq: int, ne: int, dtype=torch.float64, device=None,
+              constants: PhysicalConstants | None = None) -> "DeviceFieldState":
+        dev = _device(device)
+        dt = _torch_dtype(dtype)
+        z = dict(dtype=dt, device=dev)
+        return cls(q=torch.empty((ne, 8, nq, nq, nq), **z),
+                   rhsq=torch.zeros((ne, 8, nq, nq, nq), **z),
+                   D=torch.empty((nq, nq), **z),
+                   g=torch.empty((ne, 3, 3, nq, nq, nq), **z),
+                   Jinv=torch.empty((ne, nq, nq, nq), **z),
+                   constants=constants or PhysicalConstants())
+
+    def shard(self, start: int, stop: int) -> "DeviceFieldState":
+        """Contiguous element range [start, stop) as views (no copy): in the
+        element-batched layout each shard is one slab of every array."""
+        return DeviceFieldState(self.q[start:stop], self.rhsq[start:stop],
+                                self.D, self.g[start:stop],
+                                self.Jinv[start:stop], self.constants)
+
+    @staticmethod
+    def to_logical(x: torch.Tensor) -> np.ndarray:
+        """Element-batched (Ne, 8, k, j, i) -> numpy [i, j, k, 8, Ne]."""
+        return np.ascontiguousarray(x.permute(4, 3, 2, 1, 0).cpu().numpy())
+
+    def rhsq_logical(self) -> np.ndarray:
+        return self.to_logical(self.rhsq)
+
+
+def volume_rhs_device(ds: DeviceFieldState, *, variant="auto",
+                      stream: torch.cuda.Stream | None = None,
+                      constants: PhysicalConstants | None = None) -> None:
+    """The hot path: ``ds.rhsq += v`` on the device, one C-ABI call,
+    asynchronous on ``stream`` (default: torch's current stream)."""
+    tensors = (ds.q, ds.rhsq, ds.D, ds.g, ds.Jinv)
+    dt = ds.q.dtype
+    nq, ne = ds.nq, ds.ne
+    shapes = ((ne, 8, nq, nq, nq), (ne, 8, nq, nq, nq), (nq, nq),
+              (ne, 3, 3, nq, nq, nq), (ne, nq, nq, nq))
+    for name, t, shape in zip(("q", "rhsq", "D", "g", "Jinv"), tensors, shapes):
+        if tuple(t.shape) != shape:
+            raise ExecutionError(f"array {name!r} has shape {tuple(t.shape)}, "
+                                 f"kernel expects {shape}")
+        if t.dtype != dt:
+            raise ExecutionError(f"array {name!r} must be {dt}")
+        if t.device.type != "cuda" or t.device != ds.q.device:
+            raise ExecutionError(f"array {name!r} must be on {ds.q.device}")
+        if not t.is_contiguous():
+            raise ExecutionError(f"array {name!r} must be contiguous")
+    if dt not in (torch.float32, torch.float64):
+        raise ExecutionError(f"unsupported dtype {dt}")
+    c = constants or ds.constants
+    if stream is None:
+        stream = torch.cuda.current_stream(ds.q.device)
+    with torch.cuda.device(ds.q.device):
+        _native.volume_rhs_ptr(
+            8 if dt == torch.float64 else 4, variant, nq, ne,
+            float(c.p0), float(c.R), float(c.gamma),
+            ds.q.data_ptr(), ds.rhsq.data_ptr(), ds.D.data_ptr(),
+            ds.g.data_ptr(), ds.Jinv.data_ptr(), stream.cuda_stream)
+
+
+def volume_term(state: FieldState, c: PhysicalConstants | None = None, *,
+                dtype=np.float64, device=None, variant="auto") -> np.ndarray:
+    """The rhsq increment v at ``dtype`` (state.rhsq unchanged), logical
+    layout ``[Nq, Nq, Nq, 8, Ne]``."""
+    nq, ne = validate_state(state)
+    ds = DeviceFieldState.from_field_state(state, dtype=dtype, device=device)
+    ds.rhsq.zero_()
+    volume_rhs_device(ds, variant=variant, constants=c or state.constants)
+    return ds.rhsq_logical()
+
+
+def reference_volume_term(state: FieldState,
+                          c: PhysicalConstants | None = None) -> np.ndarray:
+    """Drop-in for ``lf/bench/reference.py:36-70``: fp64 accumulation on
+    the GPU, float32 result."""
+    return volume_term(state, c, dtype=np.float64).astype(np.float32)
+
+
+def volume_rhs_(state: FieldState, c: PhysicalConstants | None = None, *,
+                dtype=None, device=None, variant="auto") -> np.ndarray:
+    """In place ``state.rhsq += v`` (``volume.f90:53-60`` semantics),
+    computed at ``dtype`` (default: the dtype of ``state.rhsq``)."""
+    validate_state(state)
+    dt = state.rhsq.dtype if dtype is None else np.dtype(dtype)
+    ds = DeviceFieldState.from_field_state(state, dtype=dt, device=device)
+    volume_rhs_device(ds, variant=variant, constants=c or state.constants)
+    state.rhsq[...] = ds.rhsq_logical().astype(state.rhsq.dtype, copy=False)
+    return state.rhsq
+
+
+def interpret_state(kernels, state: FieldState, nq: int, ne: int,
+                    collect_counts: bool = False):
+    """Drop-in for ``lf/bench/driver.py:54-69`` with the level-8 fused
+    kernel: float32 arrays required (``lf/interp.py:71-72``), rhsq updated
+    in place, returns ``(state.rhsq, envs)`` (``envs`` is empty: there is
+    no interpreter environment). ``kernels`` is accepted for signature
+    compatibility and ignored — the CUDA kernel IS the fused kernel."""
+    validate_state(state, nq, ne, dtype=np.float32)
+    volume_rhs_(state, dtype=np.float32)
+    return state.rhsq, []
+
+
+def max_rel_error(got: np.ndarray, want: np.ndarray) -> float:
+    """Per-field max-norm relative error, worst over fields
+    (``lf/bench/driver.py:72-91``)."""
+    got64 = np.asarray(got, np.float64)
+    want64 = np.asarray(want, np.float64)
+    worst = 0.0
+    for b in range(want64.shape[3]):
+        w = want64[:, :, :, b]
+        d = np.abs(got64[:, :, :, b] - w)
+        scale = float(np.max(np.abs(w))) if w.size else 0.0
+        if scale == 0.0:
+            worst = max(worst, float(np.max(d)) if d.size else 0.0)
+        else:
+            worst = max(worst, float(np.max(d)) / scale)
+    return worst

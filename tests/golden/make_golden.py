@@ -1,0 +1,80 @@
+"""Generate the golden fixtures under tests/golden/ by importing the
+REFERENCE implementation (read-only at /root/reference/pkg/src).
+
+Run once in the build container (the reference does not exist on the GPU
+box; the fixtures travel instead):
+
+    python tests/golden/make_golden.py
+
+What it writes (``golden.npz`` + ``golden_meta.json``):
+
+* ``ref_<nq>_<ne>_<seed>``  — ``reference_volume_term(make_inputs(cfg))``
+  (f32, the reference's own output, ``lf/bench/reference.py:36-70``) for
+  small configurations, plus the SHA-256 of the f32 output bytes for the
+  larger ones (C1 = Nq=4, Ne=512 among them);
+* ``interp8_<nq>_<ne>_<seed>`` — the reference's fused level-8 kernel
+  executed by its SPMD interpreter (``interpret_state``,
+  ``lf/bench/driver.py:54-69``), f32;
+* ``inputs_sha256`` — hashes of every ``make_inputs`` array, pinning our
+  input mirror bit-exactly;
+* ``volterm_nq2_ne1_seed42`` — the reference's own golden vector
+  (``pkg/tests/golden/volterm_nq2_ne1_seed42.json``), copied as data.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import pathlib
+import sys
+
+import numpy as np
+
+REF = pathlib.Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+
+from loopforge.bench import BenchmarkConfig, make_inputs, reference_volume_term  # noqa: E402
+from loopforge.bench.driver import build_levels, interpret_state  # noqa: E402
+
+OUT = pathlib.Path(__file__).parent
+
+FULL = [(2, 1, 42), (2, 3, 1), (3, 2, 2), (3, 5, 3), (4, 5, 3), (4, 2, 6),
+        (5, 2, 4), (6, 2, 7), (7, 2, 8), (8, 3, 1), (9, 1, 2), (10, 1, 3),
+        (11, 1, 4), (12, 2, 5)]
+HASHED = [(4, 512, 1), (8, 64, 1), (8, 32, 11)]
+INTERP = [(2, 1, 1), (2, 5, 2), (3, 2, 3), (4, 2, 1)]
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def main() -> None:
+    arrays: dict[str, np.ndarray] = {}
+    meta: dict = {"full": [], "hashed": {}, "interp8": [], "inputs_sha256": {}}
+    for nq, ne, seed in FULL + HASHED:
+        st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=seed))
+        key = f"{nq}_{ne}_{seed}"
+        meta["inputs_sha256"][key] = {n: sha(a) for n, a in st.arrays().items()}
+        out = reference_volume_term(st)
+        if (nq, ne, seed) in FULL:
+            arrays[f"ref_{key}"] = out
+            meta["full"].append([nq, ne, seed])
+        else:
+            meta["hashed"][key] = sha(out)
+    for nq, ne, seed in INTERP:
+        staged = build_levels(nq, up_to=8)
+        st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=seed))
+        got, _ = interpret_state(staged[8], st.copy(), nq, ne)
+        arrays[f"interp8_{nq}_{ne}_{seed}"] = np.array(got, np.float32)
+        meta["interp8"].append([nq, ne, seed])
+    doc = json.loads((REF / "tests/golden/volterm_nq2_ne1_seed42.json").read_text())
+    arrays["volterm_nq2_ne1_seed42"] = np.array(doc["rhsq_increment"], np.float32)
+    meta["volterm_nq2_ne1_seed42_config"] = doc["config"]
+    np.savez_compressed(OUT / "golden.npz", **arrays)
+    (OUT / "golden_meta.json").write_text(json.dumps(meta, indent=1) + "\n")
+    print("wrote", len(arrays), "arrays")
+
+
+if __name__ == "__main__":
+    main()
