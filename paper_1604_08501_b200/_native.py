@@ -31,7 +31,9 @@ LFB_ERR_ALLOC = 9
 VARIANT_AUTO = 0
 VARIANT_BASIC = 1
 VARIANT_FUSED = 2
-VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED}
+VARIANT_TC = 3
+VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
+            "tc": VARIANT_TC}
 
 MAX_NQ = 16
 

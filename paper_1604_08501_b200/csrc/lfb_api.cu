@@ -17,6 +17,10 @@ int volume_fused_f64(int, int64_t, double, double, double, const double *,
 int volume_fused_f32(int, int64_t, float, float, float, const float *, float *,
                      const float *, const float *, const float *, cudaStream_t);
 bool fused_available(int dtype_bytes, int nq);
+int volume_tc_f64(int, int64_t, double, double, double, const double *, double *,
+                  const double *, const double *, const double *, cudaStream_t);
+bool tc_available(int dtype_bytes, int nq);
+bool tc_aligned(const void *q, const void *rhsq, const void *g, const void *jinv);
 }  // namespace lfb
 
 namespace {
@@ -38,9 +42,10 @@ int validate(int nq, int64_t ne, T p0, T R, T gam, const T *q, const T *rhsq,
 }
 
 int resolve(int variant, int bytes, int nq) {
-  if (variant == LFB_VARIANT_AUTO)
-    return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED
-                                           : LFB_VARIANT_BASIC;
+  if (variant == LFB_VARIANT_AUTO) {
+    if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
+    return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED : LFB_VARIANT_BASIC;
+  }
   return variant;
 }
 
@@ -55,12 +60,19 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
   int rc = validate<double>(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv);
   if (rc != LFB_OK || Ne == 0) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (resolve(variant, 8, Nq)) {
+  int v = resolve(variant, 8, Nq);
+  // AUTO never fails on alignment: misaligned arrays take the fused kernel
+  if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(q, rhsq, g, Jinv))
+    v = LFB_VARIANT_FUSED;
+  switch (v) {
     case LFB_VARIANT_BASIC:
       return lfb::volume_basic_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_FUSED:
       if (!lfb::fused_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_fused_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_TC:
+      if (!lfb::tc_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_tc_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }
@@ -107,6 +119,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return 1;
     case LFB_VARIANT_FUSED:
       return lfb::fused_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_TC:
+      return lfb::tc_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -121,6 +135,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_AUTO: return "auto";
     case LFB_VARIANT_BASIC: return "basic";
     case LFB_VARIANT_FUSED: return "fused";
+    case LFB_VARIANT_TC: return "tc";
     default: return "unknown";
   }
 }

@@ -1,0 +1,397 @@
+// LFB_VARIANT_TC — Nq = 8, fp64: TMA-staged, DMMA-contracted volume kernel.
+//
+// Why this shape (numbers from tools/microbench.cu on
+// B200): the fp64 tensor pipe (DMMA m8n8k4) has the same throughput as the
+// DFMA pipe (18.3 vs 18.4 TFMA/s) and shares it, so tensor cores do not add
+// flops here — they remove instructions, registers and shared-memory
+// traffic: one DMMA is 256 FMAs whose operand exchange happens inside the
+// tensor core, and the Nq = 8 derivative is exactly an 8x8x8 product
+// (two m8n8k4 k-steps).
+//
+// Work decomposition, one element per CTA iteration (persistent grid, one
+// CTA of 8 warps per SM):
+//   * warp w owns the (i,j)-plane k = w; lane (g = lane/4, c = lane%4) owns
+//     the points P_s = (i=g, j=c+4s, k=w), s = 0,1 — the DMMA C-fragment
+//     (row g, col 2c+s) with the column permutation pi(2c+s) = c+4s;
+//   * S (contract j): A = F_s at the thread's own points (k-index permuted
+//     the same way), B = D — no data movement;
+//   * R (contract i): B = F_r transposed in the plane — an 8x8 per-warp
+//     shared tile;
+//   * T (contract k) crosses planes, so each warp also owns the
+//     (i,k)-plane j = w ("transposed" points Q_s = (i=g, j=w, k=c+4s)):
+//     every thread evaluates F_t of all 8 fields at its own points once per
+//     element and parks them in a padded shared tile; the transposed-plane
+//     owners contract them by DMMA and hand the T result back to the
+//     (i,j)-plane owners through a second shared tile.
+//   * q and g of element e+2G are streamed into a shared stage by
+//     cp.async.bulk (TMA) with an mbarrier while element e computes; the
+//     stage is released right after phase 1, so the copy overlaps almost
+//     two element-times of compute. rhsq and Jinv of the NEXT element are
+//     prefetched into registers.
+// Traffic is exactly the 272 B/pt minimum: every q, g, Jinv, rhsq value is
+// read once and rhsq written once.
+
+#include <stdlib.h>
+
+#include "lfb_common.cuh"
+#include "lfb_math.cuh"
+
+namespace lfb {
+namespace {
+
+constexpr int TC_NQ = 8;
+constexpr int TC_NPT = 512;
+constexpr int TC_WARPS = 8;
+constexpr int TC_THREADS = 32 * TC_WARPS;
+constexpr int TC_STAGE = 17 * TC_NPT;  // doubles: q (8 fields) + g (9)
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// D += A * B on one m8n8k4 fp64 tile (A row-major 8x4, B col-major 4x8).
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Shared tiles (doubles). Plane strides are padded so every access pattern
+// below is conflict-free per half-warp (64-bit accesses are served 16 lanes
+// at a time; 128-bit ones 8 lanes at a time):
+//   ft   [field][k][j][i], k-plane stride 68: written as 16-byte pairs along
+//        i in one plane, read by the T-plane owners 4 k-planes x 4 i at a time
+//        (plane offsets 544 B = 32 B mod 128 -> distinct bank groups);
+//   tout [field][k][j][i], k-plane stride 72 (576 B = 64 B mod 128): written
+//        as pairs from 4 k-planes, read back as pairs within one plane;
+//   stile per-warp [j][i] with row stride 12 (96 B): the S transpose.
+constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
+constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
+constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
+
+template <int NS>
+struct TcSmem {
+  double stage[NS][TC_STAGE];
+  double ft[8 * FT_FS];
+  double tout[8 * TO_FS];
+  double stile[TC_WARPS][2][ST_SZ];
+  unsigned long long bar[NS];
+};
+
+__device__ __forceinline__ double2 lds2(const double *p) {
+  return *reinterpret_cast<const double2 *>(p);
+}
+__device__ __forceinline__ void sts2(double *p, double a, double b) {
+  *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+
+template <int NS, bool RHPF, bool L2PF>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    volume_tc_kernel(int64_t ne, double p0, double R, double gam, const double *__restrict__ q,
+                     double *__restrict__ rhsq, const double *__restrict__ D,
+                     const double *__restrict__ g, const double *__restrict__ jinv, int l2d) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TcSmem<NS> &sm = *reinterpret_cast<TcSmem<NS> *>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, c = lane & 3;
+  const int64_t G = gridDim.x;
+  const int64_t e0 = blockIdx.x;
+  const int64_t nmine = (e0 < ne) ? (ne - 1 - e0) / G + 1 : 0;
+  const double Rp0 = R / p0;
+
+  // Own points P_s = (i = 2c+s, j = g, k = w): the DMMA C-fragment (row g = j,
+  // cols 2c+s = i) of the warp's (i,j)-plane; a 16-byte pair in memory.
+  const int pt0 = w * 64 + gq * 8 + 2 * c;
+  const int ftW = w * FT_PS + gq * 8 + 2 * c;         // own pair in ft
+  const int toR = w * TO_PS + gq * 8 + 2 * c;         // own pair in tout
+  const int toW = gq * TO_PS + w * 8 + 2 * c;         // T result (k=g, j=w, i=2c..)
+  int ftR[2], stR[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;        // F_t(i=g, j=w, k=c+4t)
+    stR[t] = (c + 4 * t) * ST_RS + gq;                // F_s(i=g, j=c+4t)
+  }
+  const int stW = gq * ST_RS + 2 * c;                 // own F_s pair (j=g, i=2c..)
+  // D fragments (D[n*8 + i] = D(i, n)):
+  //   R: B[c][g] = D(i=g, n=2c+t);  S and T: A[g][c] = D(g, n=c+4t)
+  double Dr[2], Dst[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    Dr[t] = __ldg(D + (2 * c + t) * 8 + gq);
+    Dst[t] = __ldg(D + (c + 4 * t) * 8 + gq);
+  }
+
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm.bar);
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t n) {  // element index n (in this CTA's sequence) -> stage n % NS
+    const int s = (int)(n % NS);
+    const int64_t e = e0 + n * G;
+    mbar_expect_tx(&bars[s], TC_STAGE * sizeof(double));
+    bulk_g2s(sm.stage[s], q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double), &bars[s]);
+    bulk_g2s(sm.stage[s] + 8 * TC_NPT, g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(double), &bars[s]);
+  };
+  if (tid == 0) {
+    for (int64_t n = 0; n < NS && n < nmine; ++n) issue(n);
+  }
+  // L2 prefetch (cp.async.bulk.prefetch.L2) of the stage one beyond the
+  // shared ring and of the next element's rhsq / Jinv: keeps ~1 element per
+  // CTA (~20 MB chip-wide) in flight ahead of the TMA copies.
+  auto l2pf = [&](int64_t n) {
+    if (tid == 0 && n + NS - 1 + l2d < nmine) {
+      const int64_t e = e0 + (n + NS - 1 + l2d) * G;
+      prefetch_l2(q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double));
+      prefetch_l2(g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(double));
+    }
+    if (tid == 32 && n + l2d < nmine) {
+      const int64_t e = e0 + (n + l2d) * G;
+      prefetch_l2(rhsq + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double));
+      prefetch_l2(jinv + e * TC_NPT, TC_NPT * sizeof(double));
+    }
+  };
+
+  double2 rhn[8], jvn = make_double2(0.0, 0.0);
+  if (RHPF && nmine > 0) {
+    const double *re0 = rhsq + e0 * 8 * TC_NPT;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) rhn[b] = *reinterpret_cast<const double2 *>(re0 + b * TC_NPT + pt0);
+    jvn = __ldg(reinterpret_cast<const double2 *>(jinv + e0 * TC_NPT + pt0));
+  }
+
+  for (int64_t n = 0; n < nmine; ++n) {
+    const int st = (int)(n % NS);
+    const uint32_t parity = (uint32_t)((n / NS) & 1);
+    const int64_t e = e0 + n * G;
+    const double *sq = sm.stage[st];
+    const double *sg = sm.stage[st] + 8 * TC_NPT;
+    double *re = rhsq + e * 8 * TC_NPT;
+
+    // rhsq / Jinv of this element: only needed at write-back, so the HBM
+    // latency hides behind the whole element's compute
+    double2 rh[8], jv;
+    if (RHPF) {
+      // rotate the prefetched registers, then prefetch the next element's
+#pragma unroll
+      for (int b = 0; b < 8; ++b) rh[b] = rhn[b];
+      jv = jvn;
+      if (n + 1 < nmine) {
+        const double *rn = rhsq + (e + G) * 8 * TC_NPT;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) rhn[b] = *reinterpret_cast<const double2 *>(rn + b * TC_NPT + pt0);
+        jvn = __ldg(reinterpret_cast<const double2 *>(jinv + (e + G) * TC_NPT + pt0));
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) rh[b] = *reinterpret_cast<const double2 *>(re + b * TC_NPT + pt0);
+      jv = __ldg(reinterpret_cast<const double2 *>(jinv + e * TC_NPT + pt0));
+    }
+    if (L2PF) l2pf(n);
+
+    mbar_wait(&bars[st], parity);
+
+    // ---- phase 1: point-wise quantities of the thread's two points --------
+    double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
+    {
+      double qv[8][2], gv[9][2];
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        const double2 v = lds2(sq + f * TC_NPT + pt0);
+        qv[f][0] = v.x;
+        qv[f][1] = v.y;
+      }
+#pragma unroll
+      for (int x = 0; x < 9; ++x) {
+        const double2 v = lds2(sg + x * TC_NPT + pt0);
+        gv[x][0] = v.x;
+        gv[x][1] = v.y;
+      }
+      double V2[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double rinv = fast_rcp(qv[0][s]);
+        pP[s] = p0 * pos_pow(Rp0 * qv[4][s], gam);
+#pragma unroll
+        for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
+        V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
+        V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
+        V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gr[a][s] = gv[a][s];
+          gs[a][s] = gv[3 + a][s];
+        }
+      }
+      // F_t of every field at the own points -> ft tile
+      sts2(sm.ft + ftW, V2[0], V2[1]);
+#pragma unroll
+      for (int b = 1; b < 8; ++b) {
+        double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
+        if (b <= 3) {
+          f0 += gv[6 + (b - 1)][0] * pP[0];
+          f1 += gv[6 + (b - 1)][1] * pP[1];
+        }
+        sts2(sm.ft + b * FT_FS + ftW, f0, f1);
+      }
+    }
+    __syncthreads();  // ft complete; every stage read of this element is done
+    if (tid == 0 && n + NS < nmine) {
+      fence_proxy_async();
+      issue(n + NS);
+    }
+
+    // ---- phase 2: per field: R and S in the (i,j)-plane, T in (i,k) -----
+    double acc[8][2];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      double fr[2], fs[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (b == 0) {
+          fr[s] = V0[s];
+          fs[s] = V1[s];
+        } else {
+          fr[s] = V0[s] * sb[b][s];
+          fs[s] = V1[s] * sb[b][s];
+          if (b <= 3) {
+            fr[s] += gr[b - 1][s] * pP[s];
+            fs[s] += gs[b - 1][s] * pP[s];
+          }
+        }
+      }
+      double *stl = sm.stile[w][b & 1];
+      sts2(stl + stW, fs[0], fs[1]);
+      __syncwarp();
+      double fsT[2], ftQ[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        fsT[t] = stl[stR[t]];
+        ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
+      }
+      double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        dmma(a0, a1, fr[t], Dr[t]);    // R: A = F_r(n=2c+t, j=g), B = D(i=g, n)
+        dmma(a0, a1, Dst[t], fsT[t]);  // S: A = D(j=g, n=c+4t), B = F_s(i=g, j=n)
+        dmma(q0, q1, Dst[t], ftQ[t]);  // T: A = D(k=g, n=c+4t), B = F_t(i=g, j=w, k=n)
+      }
+      acc[b][0] = a0;
+      acc[b][1] = a1;
+      sts2(sm.tout + b * TO_FS + toW, q0, q1);
+    }
+    __syncthreads();  // tout complete
+
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const double2 t = lds2(sm.tout + b * TO_FS + toR);
+      double2 o;
+      o.x = rh[b].x + jv.x * (acc[b][0] + t.x);
+      o.y = rh[b].y + jv.y * (acc[b][1] + t.y);
+      *reinterpret_cast<double2 *>(re + b * TC_NPT + pt0) = o;
+    }
+  }
+}
+
+template <int NS, bool RHPF, bool L2PF>
+int launch_tc(int64_t ne, double p0, double R, double gam, const double *q, double *rhsq,
+              const double *D, const double *g, const double *jinv, cudaStream_t stream) {
+  const size_t smem = sizeof(TcSmem<NS>);
+  auto kern = volume_tc_kernel<NS, RHPF, L2PF>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LFB_ERR_CUDA;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return LFB_ERR_CUDA;
+  const int64_t grid = ne < sms ? ne : sms;
+  if (grid == 0) return LFB_OK;
+  static const int l2d = [] {  // L2 prefetch distance in elements (experiment knob)
+    const char *v = getenv("LFB_TC_L2D");
+    return v ? atoi(v) : 1;
+  }();
+  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ne, p0, R, gam, q, rhsq, D, g, jinv, l2d);
+  LFB_CHECK_LAUNCH();
+  return LFB_OK;
+}
+
+}  // namespace
+
+bool tc_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq == TC_NQ; }
+
+// bulk copies and 128-bit accesses need 16-byte aligned arrays
+bool tc_aligned(const void *q, const void *rhsq, const void *g, const void *jinv) {
+  return ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(rhsq) |
+           reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(jinv)) &
+          15) == 0;
+}
+
+int volume_tc_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                  double *rhsq, const double *D, const double *g, const double *jinv,
+                  cudaStream_t s) {
+  if (!tc_available(8, nq)) return LFB_ERR_BAD_VARIANT;
+  // bulk copies need 16-byte aligned element slabs
+  if (!tc_aligned(q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
+  // experiment knobs: LFB_TC_RHPF (rhsq register prefetch one element
+  // ahead), LFB_TC_L2PF (L2 bulk prefetch); defaults are the tuned choice
+  static const int rhpf = [] {
+    const char *v = getenv("LFB_TC_RHPF");
+    return v ? atoi(v) : 0;
+  }();
+  static const int l2pf = [] {
+    const char *v = getenv("LFB_TC_L2PF");
+    return v ? atoi(v) : 1;
+  }();
+  if (rhpf && l2pf) return launch_tc<2, true, true>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  if (rhpf) return launch_tc<2, true, false>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  if (l2pf) return launch_tc<2, false, true>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  return launch_tc<2, false, false>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+}  // namespace lfb

@@ -28,7 +28,7 @@ SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (3, 2, 3), (3, 33, 4), (4, 5, 3),
 
 
 def _variants(nbytes, nq):
-    return [v for v in ("basic", "fused") if _native.variant_available(v, nbytes, nq)]
+    return [v for v in ("basic", "fused", "tc") if _native.variant_available(v, nbytes, nq)]
 
 
 @pytest.mark.parametrize("nq,ne,seed", SMALL)
@@ -199,3 +199,27 @@ def test_full_size_config2_against_c_oracle(cuda_device, dtype, tol):
     err = max_rel_error(coracle.from_element_batched(got),
                         coracle.from_element_batched(want))
     assert err <= tol, err
+
+
+def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device):
+    """The TMA/DMMA kernel moves 16-byte pairs; AUTO must still accept any
+    8-byte aligned arrays (it then takes the fused kernel)."""
+    if not _native.variant_available("tc", 8, 8):
+        pytest.skip("no tc kernel")
+    st = make_inputs(BenchmarkConfig(nq=8, ne=5, seed=12))
+    want = O.volume_term_f64_batched(st)
+    ds = DeviceFieldState.from_field_state(st, dtype=torch.float64)
+    # shift every array by one double inside a bigger buffer
+    def shifted(t):
+        buf = torch.zeros(t.numel() + 1, dtype=t.dtype, device=t.device)
+        v = buf[1:].view(t.shape)
+        v.copy_(t)
+        return v
+    sh = DeviceFieldState(shifted(ds.q), shifted(ds.rhsq), ds.D, shifted(ds.g),
+                          shifted(ds.Jinv), ds.constants)
+    with pytest.raises(ExecutionError, match="aligned"):
+        volume_rhs_device(sh, variant="tc")
+    volume_rhs_device(sh, variant="auto")
+    torch.cuda.synchronize()
+    got = DeviceFieldState.to_logical(sh.rhsq)
+    assert max_rel_error(got, want) <= TOL64
