@@ -108,6 +108,28 @@ LFB_API int lfb_variant_available(int variant, int dtype_bytes, int Nq);
 LFB_API const char *lfb_variant_name(int variant);
 LFB_API int lfb_resolve_variant(int dtype_bytes, int Nq);
 
+/* --- FieldState <-> element-batched layout (device pointers) -------------
+ * The reference's numpy arrays are C-order (d0, ..., d_{ndim-1}, Ne) with the
+ * element axis fastest (lf/bench/inputs.py:52-74); the kernel layout is the
+ * full axis reversal [Ne][d_{ndim-1}]...[d0]. dims = (d0, ..., d_{ndim-1}),
+ * 1 <= ndim <= 6: q/rhsq (Nq,Nq,Nq,8), g (Nq,Nq,Nq,3,3), Jinv (Nq,Nq,Nq),
+ * D (Nq) with Ne := Nq. in/out_bytes in {4, 8}: the cast is fused. */
+LFB_API int lfb_field_state_to_element_batched(int in_bytes, int out_bytes, int ndim,
+                                               const int64_t *dims, int64_t Ne,
+                                               const void *src, void *dst, void *stream);
+LFB_API int lfb_element_batched_to_field_state(int in_bytes, int out_bytes, int ndim,
+                                               const int64_t *dims, int64_t Ne,
+                                               const void *src, void *dst, void *stream);
+
+/* --- device-side synthetic inputs (make_inputs distributions,
+ * lf/bench/inputs.py:92-112) written in the element-batched layout.
+ * Counter-based (Philox4x32-10): element e of the shard gets the values of
+ * global element e + e_offset, so shards reproduce the whole state. rhsq is
+ * zeroed; D is not touched (upload differentiation_matrix). */
+LFB_API int lfb_make_inputs_device(int Nq, int64_t Ne, int64_t e_offset, uint64_t seed,
+                                   int dtype_bytes, double p0, double Rgas, void *q,
+                                   void *rhsq, void *g, void *Jinv, void *stream);
+
 LFB_API const char *lfb_error_string(int code);
 
 /* ABI version: (major << 16) | minor. */

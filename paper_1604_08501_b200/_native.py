@@ -43,6 +43,8 @@ EXPORTED_SYMBOLS = (
     "lfb_volume_rhs_variant_f64", "lfb_volume_rhs_variant_f32",
     "lfb_variant_available", "lfb_variant_name", "lfb_resolve_variant",
     "lfb_error_string", "lfb_version",
+    "lfb_field_state_to_element_batched", "lfb_element_batched_to_field_state",
+    "lfb_make_inputs_device",
 )
 
 _lock = threading.Lock()
@@ -70,6 +72,14 @@ def _declare(L) -> None:
     L.lfb_error_string.argtypes = [_i]
     L.lfb_version.restype = _i
     L.lfb_version.argtypes = []
+    for name in ("lfb_field_state_to_element_batched",
+                 "lfb_element_batched_to_field_state"):
+        fn = getattr(L, name)
+        fn.restype = _i
+        fn.argtypes = [_i, _i, _i, ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp, _vp]
+    L.lfb_make_inputs_device.restype = _i
+    L.lfb_make_inputs_device.argtypes = [_i, _i64, _i64, ctypes.c_uint64, _i, _d, _d,
+                                         _vp, _vp, _vp, _vp, _vp]
 
 
 def lib():
@@ -132,3 +142,23 @@ def volume_rhs_ptr(dtype_bytes: int, variant, nq: int, ne: int, p0: float,
     rc = fn(variant_id(variant), int(nq), int(ne), p0, R, gam, q, rhsq, D, g,
             jinv, stream)
     check(rc, "lfb_volume_rhs")
+
+
+def reverse_axes_ptr(to_batched: bool, in_bytes: int, out_bytes: int, dims, ne: int,
+                     src: int, dst: int, stream: int) -> None:
+    """FieldState (C-order, element last) <-> element-batched conversion on
+    device pointers, with a fused f32/f64 cast."""
+    L = lib()
+    arr = (ctypes.c_int64 * len(dims))(*[int(d) for d in dims])
+    fn = (L.lfb_field_state_to_element_batched if to_batched
+          else L.lfb_element_batched_to_field_state)
+    check(fn(in_bytes, out_bytes, len(dims), arr, int(ne), src, dst, stream),
+          "layout conversion")
+
+
+def make_inputs_ptr(nq: int, ne: int, e_offset: int, seed: int, dtype_bytes: int,
+                    p0: float, R: float, q: int, rhsq: int, g: int, jinv: int,
+                    stream: int) -> None:
+    check(lib().lfb_make_inputs_device(int(nq), int(ne), int(e_offset), int(seed),
+                                       int(dtype_bytes), float(p0), float(R), q, rhsq,
+                                       g, jinv, stream), "lfb_make_inputs_device")

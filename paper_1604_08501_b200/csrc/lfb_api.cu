@@ -21,6 +21,11 @@ int volume_tc_f64(int, int64_t, double, double, double, const double *, double *
                   const double *, const double *, const double *, cudaStream_t);
 bool tc_available(int dtype_bytes, int nq);
 bool tc_aligned(const void *q, const void *rhsq, const void *g, const void *jinv);
+int reverse_axes(int to_batched, int in_bytes, int out_bytes, int ndim, const int64_t *dims,
+                 int64_t ne, const void *src, void *dst, cudaStream_t s);
+int make_inputs_device(int nq, int64_t ne, int64_t e_offset, uint64_t seed, int dtype_bytes,
+                       double p0, double R, void *q, void *rhsq, void *g, void *jinv,
+                       cudaStream_t s);
 }  // namespace lfb
 
 namespace {
@@ -156,6 +161,27 @@ const char *lfb_error_string(int code) {
   }
 }
 
-int lfb_version(void) { return (1 << 16) | 0; }
+int lfb_field_state_to_element_batched(int in_bytes, int out_bytes, int ndim,
+                                       const int64_t *dims, int64_t Ne, const void *src,
+                                       void *dst, void *stream) {
+  return lfb::reverse_axes(1, in_bytes, out_bytes, ndim, dims, Ne, src, dst,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int lfb_element_batched_to_field_state(int in_bytes, int out_bytes, int ndim,
+                                       const int64_t *dims, int64_t Ne, const void *src,
+                                       void *dst, void *stream) {
+  return lfb::reverse_axes(0, in_bytes, out_bytes, ndim, dims, Ne, src, dst,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int lfb_make_inputs_device(int Nq, int64_t Ne, int64_t e_offset, uint64_t seed,
+                           int dtype_bytes, double p0, double Rgas, void *q, void *rhsq,
+                           void *g, void *Jinv, void *stream) {
+  return lfb::make_inputs_device(Nq, Ne, e_offset, seed, dtype_bytes, p0, Rgas, q, rhsq, g,
+                                 Jinv, static_cast<cudaStream_t>(stream));
+}
+
+int lfb_version(void) { return (1 << 16) | 1; }
 
 }  // extern "C"

@@ -130,23 +130,63 @@ class DeviceFieldState:
 
     @classmethod
     def from_field_state(cls, state: FieldState, dtype=torch.float64,
-                         device=None) -> "DeviceFieldState":
-        """Upload and convert the reference's C-order arrays
-        ([i,j,k,b,e], element fastest) to the element-batched layout."""
+                         device=None, stream=None) -> "DeviceFieldState":
+        """Upload the reference's C-order arrays ([i,j,k,b,e], element
+        fastest) as they are and convert them on the device (native
+        layout kernel, cast fused) to the element-batched layout."""
         validate_state(state)
         dev = _device(device)
         dt = _torch_dtype(dtype)
+        out_bytes = 8 if dt == torch.float64 else 4
+        nq, ne = state.nq, state.ne
+        with torch.cuda.device(dev):
+            s = stream or torch.cuda.current_stream(dev)
 
-        def up(a: np.ndarray, perm):
-            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-            return t.permute(*perm).to(dt).contiguous()
+            def up(a: np.ndarray, batched_shape):
+                src = torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
+                out = torch.empty(batched_shape, dtype=dt, device=dev)
+                dims = a.shape[:-1]
+                _native.reverse_axes_ptr(True, src.element_size(), out_bytes, dims,
+                                         a.shape[-1], src.data_ptr(), out.data_ptr(),
+                                         s.cuda_stream)
+                src.record_stream(s)  # staging buffer stays valid until the kernel ran
+                return out
 
-        return cls(q=up(state.q, (4, 3, 2, 1, 0)),
-                   rhsq=up(state.rhsq, (4, 3, 2, 1, 0)),
-                   D=up(state.D, (1, 0)),
-                   g=up(state.g, (5, 4, 3, 2, 1, 0)),
-                   Jinv=up(state.Jinv, (3, 2, 1, 0)),
-                   constants=state.constants)
+            ds = cls(q=up(state.q, (ne, 8, nq, nq, nq)),
+                     rhsq=up(state.rhsq, (ne, 8, nq, nq, nq)),
+                     D=up(state.D, (nq, nq)),
+                     g=up(state.g, (ne, 3, 3, nq, nq, nq)),
+                     Jinv=up(state.Jinv, (ne, nq, nq, nq)),
+                     constants=state.constants)
+        return ds
+
+    @classmethod
+    def generate(cls, nq: int, ne: int, seed: int = 1, dtype=torch.float64,
+                 device=None, e_offset: int = 0,
+                 constants: PhysicalConstants | None = None,
+                 stream=None) -> "DeviceFieldState":
+        """Synthetic state generated on the device (make_inputs
+        distributions, counter-based RNG; element e holds global element
+        e + e_offset, so shards of a multi-GPU run reproduce one global
+        state). D is the reference's differentiation_matrix."""
+        from .inputs import differentiation_matrix
+        c = constants or PhysicalConstants()
+        ds = cls.empty(nq, ne, dtype=dtype, device=device, constants=c)
+        with torch.cuda.device(ds.device):
+            s = stream or torch.cuda.current_stream(ds.device)
+            ds.D.copy_(torch.from_numpy(differentiation_matrix(nq).T.copy()))
+            _native.make_inputs_ptr(nq, ne, e_offset, seed, ds.q.element_size(),
+                                    c.p0, c.R, ds.q.data_ptr(), ds.rhsq.data_ptr(),
+                                    ds.g.data_ptr(), ds.Jinv.data_ptr(), s.cuda_stream)
+        return ds
+
+    def to_field_state(self, dtype=None) -> FieldState:
+        """Download into the reference's logical layout (native kernel)."""
+        arrays = [self.to_logical(t, dtype) for t in (self.q, self.rhsq)]
+        D = self.to_logical(self.D, dtype)
+        g = self.to_logical(self.g, dtype)
+        J = self.to_logical(self.Jinv, dtype)
+        return FieldState(arrays[0], arrays[1], D, g, J, self.constants)
 
     @classmethod
     def empty(cls, nq: int, ne: int, dtype=torch.float64, device=None,
@@ -169,9 +209,20 @@ class DeviceFieldState:
                                 self.Jinv[start:stop], self.constants)
 
     @staticmethod
-    def to_logical(x: torch.Tensor) -> np.ndarray:
-        """Element-batched (Ne, 8, k, j, i) -> numpy [i, j, k, 8, Ne]."""
-        return np.ascontiguousarray(x.permute(4, 3, 2, 1, 0).cpu().numpy())
+    def to_logical(x: torch.Tensor, dtype=None) -> np.ndarray:
+        """Element-batched [Ne][...] tensor -> numpy C-order [..., Ne]
+        (the reference's layout), converted on the device by the native
+        layout kernel (optionally cast to ``dtype``)."""
+        dt = x.dtype if dtype is None else _torch_dtype(dtype)
+        ne = int(x.shape[0])
+        dims = tuple(int(d) for d in reversed(x.shape[1:]))
+        out = torch.empty(dims + (ne,), dtype=dt, device=x.device)
+        if x.numel():
+            with torch.cuda.device(x.device):
+                _native.reverse_axes_ptr(False, x.element_size(), out.element_size(),
+                                         dims, ne, x.data_ptr(), out.data_ptr(),
+                                         torch.cuda.current_stream(x.device).cuda_stream)
+        return out.cpu().numpy()
 
     def rhsq_logical(self) -> np.ndarray:
         return self.to_logical(self.rhsq)
