@@ -213,23 +213,40 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LFB_BENCH_SHARE_GPU=1 maps every rank to cuda:0 and uses gloo: a test
+    # mode for the multi-rank code path on a single-GPU box (not a bench)
+    share = os.environ.get("LFB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     nbytes = 8 if dt == torch.float64 else 4
     nq, ne = args.nq, args.ne
-    state = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=1 + rank))
-    ds = DeviceFieldState.from_field_state(state, dtype=dt, device=dev)
+    if args.inputs == "host":
+        state = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=1 + rank))
+        ds = DeviceFieldState.from_field_state(state, dtype=dt, device=dev)
+    else:
+        # device RNG: rank r holds global elements [r*ne, (r+1)*ne) of one state
+        state = None
+        ds = DeviceFieldState.generate(nq, ne, seed=1, dtype=dt, device=dev,
+                                       e_offset=rank * ne)
     variant = args.variant
     resolved = _native.resolve_variant(nbytes, nq) if variant == "auto" else variant
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if share:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     for _ in range(args.warmup):
         volume_rhs_device(ds, variant=variant, stream=stream)
@@ -298,6 +315,8 @@ def run_ours(args) -> None:
     checksum = global_checksum(ds.rhsq).tolist()
 
     cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and state is None:
+        state = make_inputs(BenchmarkConfig(nq=nq, ne=min(ne, 4096), seed=1))
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = host_cores()
         n = min(ne, max(cores, args.cpu_sample_per_core * cores))
@@ -337,8 +356,10 @@ def run_ours(args) -> None:
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-            "data": f"synthetic: reference make_inputs distributions "
-                    f"(seed 1+rank) upcast to {args.dtype}",
+            "data": (f"synthetic: reference make_inputs (numpy PCG64, seed 1+rank) "
+                     f"upcast to {args.dtype}" if args.inputs == "host" else
+                     f"synthetic: make_inputs distributions generated on the device "
+                     f"(Philox, seed 1, global element offset per rank), {args.dtype}"),
             "config": {"workload": f"BASELINE config {'2' if world == 1 else '3'}: "
                                    f"Nq={nq}, {ne} hex elements per GPU, "
                                    f"{args.dtype}, rhsq += v",
@@ -357,6 +378,44 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def run_sweep(args) -> None:
+    """Nq sweep at fixed ~1e8 grid points (BASELINE config 5): device
+    inputs, kernel time only, one JSON line per Nq."""
+    import torch
+    from paper_1604_08501_b200 import DeviceFieldState, volume_rhs_device
+    from paper_1604_08501_b200 import _native
+    torch.cuda.set_device(0)
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    nbytes = 8 if dt == torch.float64 else 4
+    peak, peak_src = measured_peaks()
+    for nq in range(4, 13):
+        ne = int(round(1e8 / nq ** 3))
+        ds = DeviceFieldState.generate(nq, ne, seed=1, dtype=dt)
+        variant = _native.resolve_variant(nbytes, nq)
+        for _ in range(args.warmup):
+            volume_rhs_device(ds)
+        s = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(3, min(args.steps, 50))
+        torch.cuda.synchronize()
+        a.record(s)
+        for _ in range(steps):
+            volume_rhs_device(ds)
+        b.record(s)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        pts = nq ** 3 * ne
+        gbs = bytes_per_point(nbytes) * pts / (ms * 1e-3) / 1e9
+        print(json.dumps({"sweep": True, "metric": METRIC.replace("Nq=8", f"Nq={nq}"),
+                          "nq": nq, "ne": ne, "points": pts, "dtype": args.dtype,
+                          "variant": variant, "ms_per_launch": ms,
+                          "value": pts / (ms * 1e-3) / 1e9, "unit": UNIT,
+                          "hbm_gbs": gbs, "frac": gbs / peak, "peak": peak,
+                          "peak_source": peak_src, "steps": steps}), flush=True)
+        del ds
+        torch.cuda.empty_cache()
+
+
 def main(argv=None) -> None:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -373,7 +432,14 @@ def main(argv=None) -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cpu-c", action="store_true")
     ap.add_argument("--cpu-sample-per-core", type=int, default=48)
+    ap.add_argument("--inputs", choices=("host", "device"), default="host",
+                    help="host: make_inputs (bit-identical to the reference); "
+                         "device: DeviceFieldState.generate (large configs)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE config 5: Nq 4..12 at ~1e8 DOF, one line per Nq")
     args = ap.parse_args(argv)
+    if args.sweep:
+        return run_sweep(args)
     if args.warmup < 3 and args.impl == "ours":
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":

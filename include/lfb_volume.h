@@ -80,7 +80,8 @@ enum {
     LFB_VARIANT_AUTO = 0,    /* best available for (dtype, Nq) */
     LFB_VARIANT_BASIC = 1,   /* column-per-thread, fluxes recomputed per field */
     LFB_VARIANT_FUSED = 2,   /* column-per-thread, fluxes once, register-blocked */
-    LFB_VARIANT_TC = 3       /* Nq=8 fp64: TMA-staged, DMMA (fp64 tensor core) contractions */
+    LFB_VARIANT_TC = 3       /* Nq=8: TMA-staged, DMMA (fp64 tensor core) contractions;
+                                f32 storage computes in fp64 */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -20,7 +20,10 @@ bool fused_available(int dtype_bytes, int nq);
 int volume_tc_f64(int, int64_t, double, double, double, const double *, double *,
                   const double *, const double *, const double *, cudaStream_t);
 bool tc_available(int dtype_bytes, int nq);
-bool tc_aligned(const void *q, const void *rhsq, const void *g, const void *jinv);
+int volume_tc_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                  const float *, const float *, cudaStream_t);
+bool tc_aligned(int dtype_bytes, const void *q, const void *rhsq, const void *g,
+                const void *jinv);
 int reverse_axes(int to_batched, int in_bytes, int out_bytes, int ndim, const int64_t *dims,
                  int64_t ne, const void *src, void *dst, cudaStream_t s);
 int make_inputs_device(int nq, int64_t ne, int64_t e_offset, uint64_t seed, int dtype_bytes,
@@ -67,7 +70,7 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int v = resolve(variant, 8, Nq);
   // AUTO never fails on alignment: misaligned arrays take the fused kernel
-  if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(q, rhsq, g, Jinv))
+  if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(8, q, rhsq, g, Jinv))
     v = LFB_VARIANT_FUSED;
   switch (v) {
     case LFB_VARIANT_BASIC:
@@ -90,12 +93,18 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
   int rc = validate<float>(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv);
   if (rc != LFB_OK || Ne == 0) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (resolve(variant, 4, Nq)) {
+  int v = resolve(variant, 4, Nq);
+  if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(4, q, rhsq, g, Jinv))
+    v = LFB_VARIANT_FUSED;
+  switch (v) {
     case LFB_VARIANT_BASIC:
       return lfb::volume_basic_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_FUSED:
       if (!lfb::fused_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_fused_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_TC:
+      if (!lfb::tc_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_tc_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }

@@ -1,4 +1,8 @@
-// LFB_VARIANT_TC — Nq = 8, fp64: TMA-staged, DMMA-contracted volume kernel.
+// LFB_VARIANT_TC — Nq = 8: TMA-staged, DMMA-contracted volume kernel.
+//
+// Storage type T is double (the fp64 path) or float (the fp32 variant:
+// 136 B/pt of traffic, all arithmetic still fp64 — more accurate than the
+// reference's own f32 pipeline).
 //
 // Why this shape (numbers from tools/microbench.cu on
 // B200): the fp64 tensor pipe (DMMA m8n8k4) has the same throughput as the
@@ -31,8 +35,6 @@
 // Traffic is exactly the 272 B/pt minimum: every q, g, Jinv, rhsq value is
 // read once and rhsq written once.
 
-#include <stdlib.h>
-
 #include "lfb_common.cuh"
 #include "lfb_math.cuh"
 
@@ -43,7 +45,7 @@ constexpr int TC_NQ = 8;
 constexpr int TC_NPT = 512;
 constexpr int TC_WARPS = 8;
 constexpr int TC_THREADS = 32 * TC_WARPS;
-constexpr int TC_STAGE = 17 * TC_NPT;  // doubles: q (8 fields) + g (9)
+constexpr int TC_STAGE = 17 * TC_NPT;  // values: q (8 fields) + g (9)
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -96,6 +98,38 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// A pair of adjacent values (the thread's two points) in storage type T.
+template <typename T>
+struct Pair;
+template <>
+struct Pair<double> {
+  using V = double2;
+};
+template <>
+struct Pair<float> {
+  using V = float2;
+};
+
+template <typename T>
+__device__ __forceinline__ void ld_pair(const T *p, double &a, double &b) {
+  const typename Pair<T>::V v = *reinterpret_cast<const typename Pair<T>::V *>(p);
+  a = (double)v.x;
+  b = (double)v.y;
+}
+template <typename T>
+__device__ __forceinline__ void ldg_pair(const T *p, double &a, double &b) {
+  const typename Pair<T>::V v = __ldg(reinterpret_cast<const typename Pair<T>::V *>(p));
+  a = (double)v.x;
+  b = (double)v.y;
+}
+template <typename T>
+__device__ __forceinline__ void st_pair(T *p, double a, double b) {
+  typename Pair<T>::V v;
+  v.x = (T)a;
+  v.y = (T)b;
+  *reinterpret_cast<typename Pair<T>::V *>(p) = v;
+}
+
 // Shared tiles (doubles). Plane strides are padded so every access pattern
 // below is conflict-free per half-warp (64-bit accesses are served 16 lanes
 // at a time; 128-bit ones 8 lanes at a time):
@@ -109,29 +143,26 @@ constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
 constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
 
-template <int NS>
+template <typename T, int NS>
 struct TcSmem {
-  double stage[NS][TC_STAGE];
+  T stage[NS][TC_STAGE];
   double ft[8 * FT_FS];
   double tout[8 * TO_FS];
   double stile[TC_WARPS][2][ST_SZ];
   unsigned long long bar[NS];
 };
 
-__device__ __forceinline__ double2 lds2(const double *p) {
-  return *reinterpret_cast<const double2 *>(p);
-}
 __device__ __forceinline__ void sts2(double *p, double a, double b) {
   *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-template <int NS, bool RHPF, bool L2PF>
+template <typename T, int NS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    volume_tc_kernel(int64_t ne, double p0, double R, double gam, const double *__restrict__ q,
-                     double *__restrict__ rhsq, const double *__restrict__ D,
-                     const double *__restrict__ g, const double *__restrict__ jinv, int l2d) {
+    volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
+                     T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
+                     const T *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TcSmem<NS> &sm = *reinterpret_cast<TcSmem<NS> *>(smem_raw);
+  TcSmem<T, NS> &sm = *reinterpret_cast<TcSmem<T, NS> *>(smem_raw);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
@@ -142,7 +173,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const double Rp0 = R / p0;
 
   // Own points P_s = (i = 2c+s, j = g, k = w): the DMMA C-fragment (row g = j,
-  // cols 2c+s = i) of the warp's (i,j)-plane; a 16-byte pair in memory.
+  // cols 2c+s = i) of the warp's (i,j)-plane; an adjacent pair in memory.
   const int pt0 = w * 64 + gq * 8 + 2 * c;
   const int ftW = w * FT_PS + gq * 8 + 2 * c;         // own pair in ft
   const int toR = w * TO_PS + gq * 8 + 2 * c;         // own pair in tout
@@ -159,8 +190,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   double Dr[2], Dst[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    Dr[t] = __ldg(D + (2 * c + t) * 8 + gq);
-    Dst[t] = __ldg(D + (c + 4 * t) * 8 + gq);
+    Dr[t] = (double)__ldg(D + (2 * c + t) * 8 + gq);
+    Dst[t] = (double)__ldg(D + (c + 4 * t) * 8 + gq);
   }
 
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm.bar);
@@ -174,65 +205,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   auto issue = [&](int64_t n) {  // element index n (in this CTA's sequence) -> stage n % NS
     const int s = (int)(n % NS);
     const int64_t e = e0 + n * G;
-    mbar_expect_tx(&bars[s], TC_STAGE * sizeof(double));
-    bulk_g2s(sm.stage[s], q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double), &bars[s]);
-    bulk_g2s(sm.stage[s] + 8 * TC_NPT, g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(double), &bars[s]);
+    mbar_expect_tx(&bars[s], TC_STAGE * sizeof(T));
+    bulk_g2s(sm.stage[s], q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T), &bars[s]);
+    bulk_g2s(sm.stage[s] + 8 * TC_NPT, g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(T), &bars[s]);
   };
   if (tid == 0) {
     for (int64_t n = 0; n < NS && n < nmine; ++n) issue(n);
   }
   // L2 prefetch (cp.async.bulk.prefetch.L2) of the stage one beyond the
-  // shared ring and of the next element's rhsq / Jinv: keeps ~1 element per
-  // CTA (~20 MB chip-wide) in flight ahead of the TMA copies.
+  // shared ring and of the next element's rhsq / Jinv: ~1 element per CTA
+  // (~20 MB chip-wide at fp64) in flight ahead of the TMA copies.
   auto l2pf = [&](int64_t n) {
-    if (tid == 0 && n + NS - 1 + l2d < nmine) {
-      const int64_t e = e0 + (n + NS - 1 + l2d) * G;
-      prefetch_l2(q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double));
-      prefetch_l2(g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(double));
+    if (tid == 0 && n + NS < nmine) {
+      const int64_t e = e0 + (n + NS) * G;
+      prefetch_l2(q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T));
+      prefetch_l2(g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(T));
     }
-    if (tid == 32 && n + l2d < nmine) {
-      const int64_t e = e0 + (n + l2d) * G;
-      prefetch_l2(rhsq + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(double));
-      prefetch_l2(jinv + e * TC_NPT, TC_NPT * sizeof(double));
+    if (tid == 32 && n + 1 < nmine) {
+      const int64_t e = e0 + (n + 1) * G;
+      prefetch_l2(rhsq + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T));
+      prefetch_l2(jinv + e * TC_NPT, TC_NPT * sizeof(T));
     }
   };
-
-  double2 rhn[8], jvn = make_double2(0.0, 0.0);
-  if (RHPF && nmine > 0) {
-    const double *re0 = rhsq + e0 * 8 * TC_NPT;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) rhn[b] = *reinterpret_cast<const double2 *>(re0 + b * TC_NPT + pt0);
-    jvn = __ldg(reinterpret_cast<const double2 *>(jinv + e0 * TC_NPT + pt0));
-  }
 
   for (int64_t n = 0; n < nmine; ++n) {
     const int st = (int)(n % NS);
     const uint32_t parity = (uint32_t)((n / NS) & 1);
     const int64_t e = e0 + n * G;
-    const double *sq = sm.stage[st];
-    const double *sg = sm.stage[st] + 8 * TC_NPT;
-    double *re = rhsq + e * 8 * TC_NPT;
+    const T *sq = sm.stage[st];
+    const T *sg = sm.stage[st] + 8 * TC_NPT;
+    T *re = rhsq + e * 8 * TC_NPT;
 
-    // rhsq / Jinv of this element: only needed at write-back, so the HBM
-    // latency hides behind the whole element's compute
-    double2 rh[8], jv;
-    if (RHPF) {
-      // rotate the prefetched registers, then prefetch the next element's
+    // rhsq / Jinv of this element: only needed at write-back, so the latency
+    // hides behind the element's compute (and the lines are L2-prefetched)
+    double rh[8][2], jv[2];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) rh[b] = rhn[b];
-      jv = jvn;
-      if (n + 1 < nmine) {
-        const double *rn = rhsq + (e + G) * 8 * TC_NPT;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) rhn[b] = *reinterpret_cast<const double2 *>(rn + b * TC_NPT + pt0);
-        jvn = __ldg(reinterpret_cast<const double2 *>(jinv + (e + G) * TC_NPT + pt0));
-      }
-    } else {
-#pragma unroll
-      for (int b = 0; b < 8; ++b) rh[b] = *reinterpret_cast<const double2 *>(re + b * TC_NPT + pt0);
-      jv = __ldg(reinterpret_cast<const double2 *>(jinv + e * TC_NPT + pt0));
-    }
-    if (L2PF) l2pf(n);
+    for (int b = 0; b < 8; ++b) ld_pair(re + b * TC_NPT + pt0, rh[b][0], rh[b][1]);
+    ldg_pair(jinv + e * TC_NPT + pt0, jv[0], jv[1]);
+    l2pf(n);
 
     mbar_wait(&bars[st], parity);
 
@@ -241,17 +251,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     {
       double qv[8][2], gv[9][2];
 #pragma unroll
-      for (int f = 0; f < 8; ++f) {
-        const double2 v = lds2(sq + f * TC_NPT + pt0);
-        qv[f][0] = v.x;
-        qv[f][1] = v.y;
-      }
+      for (int f = 0; f < 8; ++f) ld_pair(sq + f * TC_NPT + pt0, qv[f][0], qv[f][1]);
 #pragma unroll
-      for (int x = 0; x < 9; ++x) {
-        const double2 v = lds2(sg + x * TC_NPT + pt0);
-        gv[x][0] = v.x;
-        gv[x][1] = v.y;
-      }
+      for (int x = 0; x < 9; ++x) ld_pair(sg + x * TC_NPT + pt0, gv[x][0], gv[x][1]);
       double V2[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -329,20 +331,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const double2 t = lds2(sm.tout + b * TO_FS + toR);
-      double2 o;
-      o.x = rh[b].x + jv.x * (acc[b][0] + t.x);
-      o.y = rh[b].y + jv.y * (acc[b][1] + t.y);
-      *reinterpret_cast<double2 *>(re + b * TC_NPT + pt0) = o;
+      const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
+      st_pair(re + b * TC_NPT + pt0, rh[b][0] + jv[0] * (acc[b][0] + t.x),
+              rh[b][1] + jv[1] * (acc[b][1] + t.y));
     }
   }
 }
 
-template <int NS, bool RHPF, bool L2PF>
-int launch_tc(int64_t ne, double p0, double R, double gam, const double *q, double *rhsq,
-              const double *D, const double *g, const double *jinv, cudaStream_t stream) {
-  const size_t smem = sizeof(TcSmem<NS>);
-  auto kern = volume_tc_kernel<NS, RHPF, L2PF>;
+template <typename T, int NS>
+int launch_tc(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, const T *D,
+              const T *g, const T *jinv, cudaStream_t stream) {
+  const size_t smem = sizeof(TcSmem<T, NS>);
+  auto kern = volume_tc_kernel<T, NS>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
@@ -352,46 +352,40 @@ int launch_tc(int64_t ne, double p0, double R, double gam, const double *q, doub
     return LFB_ERR_CUDA;
   const int64_t grid = ne < sms ? ne : sms;
   if (grid == 0) return LFB_OK;
-  static const int l2d = [] {  // L2 prefetch distance in elements (experiment knob)
-    const char *v = getenv("LFB_TC_L2D");
-    return v ? atoi(v) : 1;
-  }();
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ne, p0, R, gam, q, rhsq, D, g, jinv, l2d);
+  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
 
 }  // namespace
 
-bool tc_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq == TC_NQ; }
+bool tc_available(int dtype_bytes, int nq) {
+  return (dtype_bytes == 8 || dtype_bytes == 4) && nq == TC_NQ;
+}
 
-// bulk copies and 128-bit accesses need 16-byte aligned arrays
-bool tc_aligned(const void *q, const void *rhsq, const void *g, const void *jinv) {
-  return ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(rhsq) |
-           reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(jinv)) &
-          15) == 0;
+// bulk copies need 16-byte aligned q and g element slabs; the paired
+// accesses need rhsq / Jinv aligned to two elements
+bool tc_aligned(int dtype_bytes, const void *q, const void *rhsq, const void *g,
+                const void *jinv) {
+  const uintptr_t pair = 2 * (uintptr_t)dtype_bytes - 1;
+  return (((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(g)) & 15) == 0) &&
+         (((reinterpret_cast<uintptr_t>(rhsq) | reinterpret_cast<uintptr_t>(jinv)) & pair) == 0);
 }
 
 int volume_tc_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
                   double *rhsq, const double *D, const double *g, const double *jinv,
                   cudaStream_t s) {
   if (!tc_available(8, nq)) return LFB_ERR_BAD_VARIANT;
-  // bulk copies need 16-byte aligned element slabs
-  if (!tc_aligned(q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
-  // experiment knobs: LFB_TC_RHPF (rhsq register prefetch one element
-  // ahead), LFB_TC_L2PF (L2 bulk prefetch); defaults are the tuned choice
-  static const int rhpf = [] {
-    const char *v = getenv("LFB_TC_RHPF");
-    return v ? atoi(v) : 0;
-  }();
-  static const int l2pf = [] {
-    const char *v = getenv("LFB_TC_L2PF");
-    return v ? atoi(v) : 1;
-  }();
-  if (rhpf && l2pf) return launch_tc<2, true, true>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-  if (rhpf) return launch_tc<2, true, false>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-  if (l2pf) return launch_tc<2, false, true>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-  return launch_tc<2, false, false>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  if (!tc_aligned(8, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
+  return launch_tc<double, 2>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
+                  float *rhsq, const float *D, const float *g, const float *jinv,
+                  cudaStream_t s) {
+  if (!tc_available(4, nq)) return LFB_ERR_BAD_VARIANT;
+  if (!tc_aligned(4, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
+  return launch_tc<float, 3>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
 }  // namespace lfb
