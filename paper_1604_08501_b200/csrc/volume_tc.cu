@@ -130,25 +130,32 @@ __device__ __forceinline__ void st_pair(T *p, double a, double b) {
   *reinterpret_cast<typename Pair<T>::V *>(p) = v;
 }
 
-// Shared tiles (doubles). Plane strides are padded so every access pattern
-// below is conflict-free per half-warp (64-bit accesses are served 16 lanes
-// at a time; 128-bit ones 8 lanes at a time):
-//   ft   [field][k][j][i], k-plane stride 68: written as 16-byte pairs along
-//        i in one plane, read by the T-plane owners 4 k-planes x 4 i at a time
-//        (plane offsets 544 B = 32 B mod 128 -> distinct bank groups);
-//   tout [field][k][j][i], k-plane stride 72 (576 B = 64 B mod 128): written
-//        as pairs from 4 k-planes, read back as pairs within one plane;
-//   stile per-warp [j][i] with row stride 12 (96 B): the S transpose.
+// Shared tiles (doubles), laid out so every access below is conflict-free
+// per half-warp (64-bit accesses are served 16 lanes at a time, 128-bit ones
+// 8 lanes at a time):
+//   ft [field][k][j][i], k-plane stride 68: F_t written as 16-byte pairs
+//      along i in one plane, read by the (i,k)-plane owners 4 k-planes x 4 i
+//      at a time (plane offsets 544 B = 32 B mod 128: distinct bank groups);
+//   fs [field][k][j][i], plane stride 64, 16-byte chunk index XOR
+//      2*((j>>1)&1): F_s written as pairs along i (4 rows of a plane), read
+//      transposed (4 rows j = c+4t x 4 consecutive i);
+//   tout [field][k][j][i], k-plane stride 72 (576 B = 64 B mod 128): T
+//      results written as pairs from 4 k-planes, read back within one plane.
+//      tout reuses fs's storage (fs is dead once the DMMA operands are in
+//      registers; a barrier separates the two).
 constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
+constexpr int FS_FS = 512;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
-constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
+
+__device__ __forceinline__ int fs_at(int k, int j, int i) {
+  return k * 64 + j * 8 + (((i >> 1) ^ (((j >> 1) & 1) << 1)) << 1) + (i & 1);
+}
 
 template <typename T, int NS>
 struct TcSmem {
   T stage[NS][TC_STAGE];
   double ft[8 * FT_FS];
-  double tout[8 * TO_FS];
-  double stile[TC_WARPS][2][ST_SZ];
+  double fs_tout[8 * TO_FS];  // fs [8*FS_FS] then, after a barrier, tout [8*TO_FS]
   unsigned long long bar[NS];
 };
 
@@ -175,16 +182,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // Own points P_s = (i = 2c+s, j = g, k = w): the DMMA C-fragment (row g = j,
   // cols 2c+s = i) of the warp's (i,j)-plane; an adjacent pair in memory.
   const int pt0 = w * 64 + gq * 8 + 2 * c;
-  const int ftW = w * FT_PS + gq * 8 + 2 * c;         // own pair in ft
-  const int toR = w * TO_PS + gq * 8 + 2 * c;         // own pair in tout
-  const int toW = gq * TO_PS + w * 8 + 2 * c;         // T result (k=g, j=w, i=2c..)
-  int ftR[2], stR[2];
+  const int ftW = w * FT_PS + gq * 8 + 2 * c;          // own pair in ft
+  const int fsW = fs_at(w, gq, 2 * c);                 // own pair in fs
+  const int toR = w * TO_PS + gq * 8 + 2 * c;          // own pair in tout
+  const int toW = gq * TO_PS + w * 8 + 2 * c;          // T result (k=g, j=w, i=2c..)
+  int ftR[2], fsR[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;        // F_t(i=g, j=w, k=c+4t)
-    stR[t] = (c + 4 * t) * ST_RS + gq;                // F_s(i=g, j=c+4t)
+    ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;         // F_t(i=g, j=w, k=c+4t)
+    fsR[t] = fs_at(w, c + 4 * t, gq);                  // F_s(i=g, j=c+4t, k=w)
   }
-  const int stW = gq * ST_RS + 2 * c;                 // own F_s pair (j=g, i=2c..)
   // D fragments (D[n*8 + i] = D(i, n)):
   //   R: B[c][g] = D(i=g, n=2c+t);  S and T: A[g][c] = D(g, n=c+4t)
   double Dr[2], Dst[2];
@@ -246,95 +253,86 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     mbar_wait(&bars[st], parity);
 
-    // ---- phase 1: point-wise quantities of the thread's two points --------
-    double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
+    // ---- phase 1: point-wise work at the thread's two points --------------
+    // F_r of every field stays in registers; F_s and F_t of every field go
+    // to the shared tiles for the transposed readers.
+    double fr[8][2];
     {
       double qv[8][2], gv[9][2];
 #pragma unroll
       for (int f = 0; f < 8; ++f) ld_pair(sq + f * TC_NPT + pt0, qv[f][0], qv[f][1]);
 #pragma unroll
       for (int x = 0; x < 9; ++x) ld_pair(sg + x * TC_NPT + pt0, gv[x][0], gv[x][1]);
-      double V2[2];
+      double sb[8][2], V[3][2], pP[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const double rinv = fast_rcp(qv[0][s]);
         pP[s] = p0 * pos_pow(Rp0 * qv[4][s], gam);
 #pragma unroll
         for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
-        V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
-        V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
-        V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          gr[a][s] = gv[a][s];
-          gs[a][s] = gv[3 + a][s];
-        }
+        for (int d = 0; d < 3; ++d)
+          V[d][s] = gv[3 * d + 0][s] * qv[1][s] + gv[3 * d + 1][s] * qv[2][s] +
+                    gv[3 * d + 2][s] * qv[3][s];
       }
-      // F_t of every field at the own points -> ft tile
-      sts2(sm.ft + ftW, V2[0], V2[1]);
 #pragma unroll
-      for (int b = 1; b < 8; ++b) {
-        double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
-        if (b <= 3) {
-          f0 += gv[6 + (b - 1)][0] * pP[0];
-          f1 += gv[6 + (b - 1)][1] * pP[1];
+      for (int b = 0; b < 8; ++b) {
+        double f[3][2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            f[d][s] = (b == 0) ? V[d][s] : V[d][s] * sb[b][s];
+            if (b >= 1 && b <= 3) f[d][s] += gv[3 * d + (b - 1)][s] * pP[s];
+          }
+          fr[b][s] = f[0][s];
         }
-        sts2(sm.ft + b * FT_FS + ftW, f0, f1);
+        sts2(sm.fs_tout + b * FS_FS + fsW, f[1][0], f[1][1]);
+        sts2(sm.ft + b * FT_FS + ftW, f[2][0], f[2][1]);
       }
     }
-    __syncthreads();  // ft complete; every stage read of this element is done
+    __syncthreads();  // (1) fs/ft complete; every stage read of this element done
     if (tid == 0 && n + NS < nmine) {
       fence_proxy_async();
       issue(n + NS);
     }
 
-    // ---- phase 2: per field: R and S in the (i,j)-plane, T in (i,k) -----
-    double acc[8][2];
+    // ---- phase 2: all 8 fields' contractions, no barrier in between -------
+    double fsT[8][2], ftQ[8][2];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      double fr[2], fs[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (b == 0) {
-          fr[s] = V0[s];
-          fs[s] = V1[s];
-        } else {
-          fr[s] = V0[s] * sb[b][s];
-          fs[s] = V1[s] * sb[b][s];
-          if (b <= 3) {
-            fr[s] += gr[b - 1][s] * pP[s];
-            fs[s] += gs[b - 1][s] * pP[s];
-          }
-        }
-      }
-      double *stl = sm.stile[w][b & 1];
-      sts2(stl + stW, fs[0], fs[1]);
-      __syncwarp();
-      double fsT[2], ftQ[2];
+    for (int b = 0; b < 8; ++b)
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        fsT[t] = stl[stR[t]];
-        ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
+        fsT[b][t] = sm.fs_tout[b * FS_FS + fsR[t]];
+        ftQ[b][t] = sm.ft[b * FT_FS + ftR[t]];
       }
+    double acc[8][2], tq[8][2];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
       double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        dmma(a0, a1, fr[t], Dr[t]);    // R: A = F_r(n=2c+t, j=g), B = D(i=g, n)
-        dmma(a0, a1, Dst[t], fsT[t]);  // S: A = D(j=g, n=c+4t), B = F_s(i=g, j=n)
-        dmma(q0, q1, Dst[t], ftQ[t]);  // T: A = D(k=g, n=c+4t), B = F_t(i=g, j=w, k=n)
+        dmma(a0, a1, fr[b][t], Dr[t]);    // R: A = F_r(n=2c+t, j=g), B = D(i=g, n)
+        dmma(a0, a1, Dst[t], fsT[b][t]);  // S: A = D(j=g, n=c+4t), B = F_s(i=g, j=n)
+        dmma(q0, q1, Dst[t], ftQ[b][t]);  // T: A = D(k=g, n=c+4t), B = F_t(i=g, j=w, k=n)
       }
       acc[b][0] = a0;
       acc[b][1] = a1;
-      sts2(sm.tout + b * TO_FS + toW, q0, q1);
+      tq[b][0] = q0;
+      tq[b][1] = q1;
     }
-    __syncthreads();  // tout complete
+    __syncthreads();  // (2) every fs read done: fs storage becomes tout
+#pragma unroll
+    for (int b = 0; b < 8; ++b) sts2(sm.fs_tout + b * TO_FS + toW, tq[b][0], tq[b][1]);
+    __syncthreads();  // (3) tout complete
 
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
+      const double2 t = *reinterpret_cast<const double2 *>(sm.fs_tout + b * TO_FS + toR);
       st_pair(re + b * TC_NPT + pt0, rh[b][0] + jv[0] * (acc[b][0] + t.x),
               rh[b][1] + jv[1] * (acc[b][1] + t.y));
     }
+    __syncthreads();  // (4) tout reads done before the next element's fs writes
   }
 }
 
