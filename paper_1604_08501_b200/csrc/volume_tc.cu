@@ -35,10 +35,23 @@
 // Traffic is exactly the 272 B/pt minimum: every q, g, Jinv, rhsq value is
 // read once and rhsq written once.
 
+#include <stdlib.h>
+
 #include "lfb_common.cuh"
 #include "lfb_math.cuh"
 
 namespace lfb {
+
+int volume_basic_f64(int, int64_t, double, double, double, const double *, double *,
+                     const double *, const double *, const double *, cudaStream_t);
+int volume_basic_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                     const float *, const float *, cudaStream_t);
+int volume_fused_f64(int, int64_t, double, double, double, const double *, double *,
+                     const double *, const double *, const double *, cudaStream_t);
+int volume_fused_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                     const float *, const float *, cudaStream_t);
+bool fused_available(int dtype_bytes, int nq);
+
 namespace {
 
 constexpr int TC_NQ = 8;
@@ -151,19 +164,50 @@ __device__ __forceinline__ int fs_at(int k, int j, int i) {
   return k * 64 + j * 8 + (((i >> 1) ^ (((j >> 1) & 1) << 1)) << 1) + (i & 1);
 }
 
+constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;  // per-warp [j][i] S tile, row stride 96 B
+
 template <typename T, int NS>
 struct TcSmem {
   T stage[NS][TC_STAGE];
   double ft[8 * FT_FS];
   double fs_tout[8 * TO_FS];  // fs [8*FS_FS] then, after a barrier, tout [8*TO_FS]
+  double stile[TC_WARPS][2][ST_SZ];  // PERFIELD variant only
   unsigned long long bar[NS];
 };
+
+// 1/rho and p = p0 (R Theta / p0)^gam of one point. fp32 storage
+// (tolerance 1e-5): both in the FP32 pipe (MUFU rcp/lg2/ex2, ~5e-7
+// relative); the fluxes and the contractions stay fp64.
+template <typename T>
+__device__ __forceinline__ void point_scalars(double rho, double th, double p0, double Rp0,
+                                              double gam, double &rinv, double &p) {
+  if constexpr (sizeof(T) == 4) {
+    rinv = (double)__frcp_rn((float)rho);
+    p = p0 * (double)exp2f((float)gam * log2f((float)Rp0 * (float)th));
+  } else {
+    rinv = fast_rcp(rho);
+    p = p0 * pos_pow(Rp0 * th, gam);
+  }
+}
 
 __device__ __forceinline__ void sts2(double *p, double a, double b) {
   *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-template <typename T, int NS>
+// PERFIELD = true: phase 2 walks the fields one at a time, F_s transposed
+// through a per-warp tile (__syncwarp only), T results exchanged through
+// tout, 2 CTA barriers per element. PERFIELD = false: F_s of all fields
+// goes through an element-wide tile written in phase 1, all 48 DMMAs of an
+// element are independent, 4 CTA barriers per element.
+// SUB = the real Nq. SUB = 8: one element per iteration. SUB = 4 or 2: a
+// "virtual" Nq=8 element packs P^3 real elements (P = 8/SUB) — virtual point
+// (i + SUB a, j + SUB b, k + SUB c) is point (i,j,k) of real element
+// a + P b + P^2 c of the group — and the virtual D is blockdiag(D, ..., D),
+// so the Nq=8 contraction machinery computes P^3 independent elements.
+// A group of P^3 consecutive elements is the same 8*512 / 9*512 value slab
+// as one Nq=8 element, so the TMA and prefetch code is unchanged; only the
+// thread's own-point offsets inside the slab differ. `ne` counts groups.
+template <typename T, int NS, bool PERFIELD, int SUB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
@@ -181,7 +225,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   // Own points P_s = (i = 2c+s, j = g, k = w): the DMMA C-fragment (row g = j,
   // cols 2c+s = i) of the warp's (i,j)-plane; an adjacent pair in memory.
-  const int pt0 = w * 64 + gq * 8 + 2 * c;
+  constexpr int P = 8 / SUB, NPTR = SUB * SUB * SUB;
+  static_assert(SUB == 8 || SUB == 4 || SUB == 2, "packing needs SUB | 8, SUB even");
+  // own pair (virtual i = 2c, 2c+1; j = g; k = w) inside the group's slabs
+  const int ur = (2 * c) / SUB + P * (gq / SUB) + P * P * (w / SUB);   // real element
+  const int ptr = ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;  // real point
+  const int qo = ur * 8 * NPTR + ptr;  // q / rhsq field 0; fields stride NPTR
+  const int go = ur * 9 * NPTR + ptr;  // g component 0; components stride NPTR
+  const int jo = ur * NPTR + ptr;      // Jinv
   const int ftW = w * FT_PS + gq * 8 + 2 * c;          // own pair in ft
   const int fsW = fs_at(w, gq, 2 * c);                 // own pair in fs
   const int toR = w * TO_PS + gq * 8 + 2 * c;          // own pair in tout
@@ -194,11 +245,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   // D fragments (D[n*8 + i] = D(i, n)):
   //   R: B[c][g] = D(i=g, n=2c+t);  S and T: A[g][c] = D(g, n=c+4t)
+  // (virtual D = blockdiag of the real D for SUB < 8)
+  auto Dv = [&](int iv, int nv) -> double {
+    if (iv / SUB != nv / SUB) return 0.0;
+    return (double)__ldg(D + (nv % SUB) * SUB + (iv % SUB));
+  };
   double Dr[2], Dst[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    Dr[t] = (double)__ldg(D + (2 * c + t) * 8 + gq);
-    Dst[t] = (double)__ldg(D + (c + 4 * t) * 8 + gq);
+    Dr[t] = Dv(gq, 2 * c + t);
+    Dst[t] = Dv(gq, c + 4 * t);
   }
 
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm.bar);
@@ -247,11 +303,101 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // hides behind the element's compute (and the lines are L2-prefetched)
     double rh[8][2], jv[2];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) ld_pair(re + b * TC_NPT + pt0, rh[b][0], rh[b][1]);
-    ldg_pair(jinv + e * TC_NPT + pt0, jv[0], jv[1]);
+    for (int b = 0; b < 8; ++b) ld_pair(re + qo + b * NPTR, rh[b][0], rh[b][1]);
+    ldg_pair(jinv + e * TC_NPT + jo, jv[0], jv[1]);
     l2pf(n);
 
     mbar_wait(&bars[st], parity);
+
+    if constexpr (PERFIELD) {
+      // ---- phase 1: point-wise quantities of the thread's two points ------
+      double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
+      {
+        double qv[8][2], gv[9][2];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
+#pragma unroll
+        for (int x = 0; x < 9; ++x) ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
+        double V2[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          double rinv;
+          point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
+#pragma unroll
+          for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
+          V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
+          V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
+          V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            gr[a][s] = gv[a][s];
+            gs[a][s] = gv[3 + a][s];
+          }
+        }
+        sts2(sm.ft + ftW, V2[0], V2[1]);
+#pragma unroll
+        for (int b = 1; b < 8; ++b) {
+          double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
+          if (b <= 3) {
+            f0 += gv[6 + (b - 1)][0] * pP[0];
+            f1 += gv[6 + (b - 1)][1] * pP[1];
+          }
+          sts2(sm.ft + b * FT_FS + ftW, f0, f1);
+        }
+      }
+      __syncthreads();  // ft complete; every stage read of this element is done
+      if (tid == 0 && n + NS < nmine) {
+        fence_proxy_async();
+        issue(n + NS);
+      }
+      // ---- phase 2: per field ----------------------------------------------
+      double acc[8][2];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        double fr[2], fs[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (b == 0) {
+            fr[s] = V0[s];
+            fs[s] = V1[s];
+          } else {
+            fr[s] = V0[s] * sb[b][s];
+            fs[s] = V1[s] * sb[b][s];
+            if (b <= 3) {
+              fr[s] += gr[b - 1][s] * pP[s];
+              fs[s] += gs[b - 1][s] * pP[s];
+            }
+          }
+        }
+        double *stl = sm.stile[w][b & 1];
+        sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
+        __syncwarp();
+        double fsT[2], ftQ[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
+          ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
+        }
+        double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          dmma(a0, a1, fr[t], Dr[t]);
+          dmma(a0, a1, Dst[t], fsT[t]);
+          dmma(q0, q1, Dst[t], ftQ[t]);
+        }
+        acc[b][0] = a0;
+        acc[b][1] = a1;
+        sts2(sm.fs_tout + b * TO_FS + toW, q0, q1);
+      }
+      __syncthreads();  // tout complete
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const double2 t = *reinterpret_cast<const double2 *>(sm.fs_tout + b * TO_FS + toR);
+        st_pair(re + qo + b * NPTR, rh[b][0] + jv[0] * (acc[b][0] + t.x),
+                rh[b][1] + jv[1] * (acc[b][1] + t.y));
+      }
+      continue;
+    }
 
     // ---- phase 1: point-wise work at the thread's two points --------------
     // F_r of every field stays in registers; F_s and F_t of every field go
@@ -260,14 +406,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     {
       double qv[8][2], gv[9][2];
 #pragma unroll
-      for (int f = 0; f < 8; ++f) ld_pair(sq + f * TC_NPT + pt0, qv[f][0], qv[f][1]);
+      for (int f = 0; f < 8; ++f) ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
 #pragma unroll
-      for (int x = 0; x < 9; ++x) ld_pair(sg + x * TC_NPT + pt0, gv[x][0], gv[x][1]);
+      for (int x = 0; x < 9; ++x) ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
       double sb[8][2], V[3][2], pP[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const double rinv = fast_rcp(qv[0][s]);
-        pP[s] = p0 * pos_pow(Rp0 * qv[4][s], gam);
+        double rinv;
+        point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
 #pragma unroll
         for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
 #pragma unroll
@@ -329,18 +475,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const double2 t = *reinterpret_cast<const double2 *>(sm.fs_tout + b * TO_FS + toR);
-      st_pair(re + b * TC_NPT + pt0, rh[b][0] + jv[0] * (acc[b][0] + t.x),
+      st_pair(re + qo + b * NPTR, rh[b][0] + jv[0] * (acc[b][0] + t.x),
               rh[b][1] + jv[1] * (acc[b][1] + t.y));
     }
     __syncthreads();  // (4) tout reads done before the next element's fs writes
   }
 }
 
-template <typename T, int NS>
-int launch_tc(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, const T *D,
-              const T *g, const T *jinv, cudaStream_t stream) {
+template <typename T, int NS, int SUB>
+int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
+              const T *D, const T *g, const T *jinv, cudaStream_t stream) {
   const size_t smem = sizeof(TcSmem<T, NS>);
-  auto kern = volume_tc_kernel<T, NS>;
+  static const int perfield = [] {  // A/B knob: LFB_TC_PERFIELD=0|1
+    const char *v = getenv("LFB_TC_PERFIELD");
+    return v ? atoi(v) : 1;
+  }();
+  auto kern = perfield ? volume_tc_kernel<T, NS, true, SUB> : volume_tc_kernel<T, NS, false, SUB>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
@@ -348,17 +498,56 @@ int launch_tc(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, 
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return LFB_ERR_CUDA;
-  const int64_t grid = ne < sms ? ne : sms;
+  const int64_t grid = ngroups < sms ? ngroups : sms;
   if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
+}
+
+template <typename T>
+int tail_launch(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
+                const T *g, const T *jinv, cudaStream_t s);
+
+template <>
+int tail_launch<double>(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                        double *rhsq, const double *D, const double *g, const double *jinv,
+                        cudaStream_t s) {
+  return fused_available(8, nq) ? volume_fused_f64(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s)
+                                : volume_basic_f64(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+template <>
+int tail_launch<float>(int nq, int64_t ne, float p0, float R, float gam, const float *q,
+                       float *rhsq, const float *D, const float *g, const float *jinv,
+                       cudaStream_t s) {
+  return fused_available(4, nq) ? volume_fused_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s)
+                                : volume_basic_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+// Full groups of P^3 elements go through the packed tensor-core kernel; the
+// < P^3 leftover elements (Nq = 4: < 8, Nq = 2: < 64) take the fused/basic
+// kernel on the same stream.
+template <typename T, int NS>
+int dispatch_tc(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
+                const T *g, const T *jinv, cudaStream_t s) {
+  const int64_t pe = (int64_t)(8 / nq) * (8 / nq) * (8 / nq);
+  const int64_t groups = ne / pe, done = groups * pe, npt = (int64_t)nq * nq * nq;
+  int rc = LFB_OK;
+  if (groups > 0) {
+    if (nq == 8) rc = launch_tc<T, NS, 8>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+    else if (nq == 4) rc = launch_tc<T, NS, 4>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+    else rc = launch_tc<T, NS, 2>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+  }
+  if (rc != LFB_OK || done == ne) return rc;
+  return tail_launch<T>(nq, ne - done, p0, R, gam, q + done * 8 * npt, rhsq + done * 8 * npt,
+                        D, g + done * 9 * npt, jinv + done * npt, s);
 }
 
 }  // namespace
 
 bool tc_available(int dtype_bytes, int nq) {
-  return (dtype_bytes == 8 || dtype_bytes == 4) && nq == TC_NQ;
+  return (dtype_bytes == 8 || dtype_bytes == 4) && (nq == 8 || nq == 4 || nq == 2);
 }
 
 // bulk copies need 16-byte aligned q and g element slabs; the paired
@@ -375,7 +564,7 @@ int volume_tc_f64(int nq, int64_t ne, double p0, double R, double gam, const dou
                   cudaStream_t s) {
   if (!tc_available(8, nq)) return LFB_ERR_BAD_VARIANT;
   if (!tc_aligned(8, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
-  return launch_tc<double, 2>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  return dispatch_tc<double, 2>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
 int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
@@ -383,7 +572,7 @@ int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float 
                   cudaStream_t s) {
   if (!tc_available(4, nq)) return LFB_ERR_BAD_VARIANT;
   if (!tc_aligned(4, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
-  return launch_tc<float, 3>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  return dispatch_tc<float, 3>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
 }  // namespace lfb

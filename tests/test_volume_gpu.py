@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 TOL64 = 1e-12
 TOL32 = 1e-5
 
-SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (3, 2, 3), (3, 33, 4), (4, 5, 3),
+SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (2, 130, 3), (3, 2, 3), (3, 33, 4), (4, 5, 3),
+         (4, 37, 5), (4, 8, 2),
          (4, 17, 6), (5, 3, 4), (6, 7, 7), (7, 2, 8), (8, 3, 1), (8, 13, 9),
          (9, 2, 2), (10, 2, 3), (11, 1, 4), (12, 3, 5), (13, 1, 6), (16, 2, 7)]
 
@@ -223,3 +224,18 @@ def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device):
     torch.cuda.synchronize()
     got = DeviceFieldState.to_logical(sh.rhsq)
     assert max_rel_error(got, want) <= TOL64
+
+
+@pytest.mark.parametrize("nq,ne", [(4, 8 * 300 + 3), (2, 64 * 20 + 17)])
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, TOL64), (torch.float32, TOL32)])
+def test_packed_tc_groups_and_tail_against_c_oracle(cuda_device, nq, ne, dtype, tol):
+    """Nq = 4 / 2 run as packed virtual Nq=8 elements (blockdiag D) plus a
+    fused/basic tail; every element against the C oracle."""
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=8))
+    ds = DeviceFieldState.from_field_state(st, dtype=dtype)
+    volume_rhs_device(ds, variant="tc")
+    got = ds.rhsq.to(torch.float64).cpu().numpy()
+    q, g, j, d = coracle.to_element_batched(st)
+    want = coracle.volume_f64_eb(nq, q, g, j, d, st.constants)
+    err = max_rel_error(coracle.from_element_batched(got), coracle.from_element_batched(want))
+    assert err <= tol, err
