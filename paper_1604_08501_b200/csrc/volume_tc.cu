@@ -149,29 +149,19 @@ __device__ __forceinline__ void st_pair(T *p, double a, double b) {
 //   ft [field][k][j][i], k-plane stride 68: F_t written as 16-byte pairs
 //      along i in one plane, read by the (i,k)-plane owners 4 k-planes x 4 i
 //      at a time (plane offsets 544 B = 32 B mod 128: distinct bank groups);
-//   fs [field][k][j][i], plane stride 64, 16-byte chunk index XOR
-//      2*((j>>1)&1): F_s written as pairs along i (4 rows of a plane), read
-//      transposed (4 rows j = c+4t x 4 consecutive i);
 //   tout [field][k][j][i], k-plane stride 72 (576 B = 64 B mod 128): T
-//      results written as pairs from 4 k-planes, read back within one plane.
-//      tout reuses fs's storage (fs is dead once the DMMA operands are in
-//      registers; a barrier separates the two).
+//      results written as pairs from 4 k-planes, read back within one plane;
+//   stile per-warp [j][i], row stride 12 (96 B): the in-plane S transpose.
 constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
-constexpr int FS_FS = 512;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
-
-__device__ __forceinline__ int fs_at(int k, int j, int i) {
-  return k * 64 + j * 8 + (((i >> 1) ^ (((j >> 1) & 1) << 1)) << 1) + (i & 1);
-}
-
-constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;  // per-warp [j][i] S tile, row stride 96 B
+constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
 
 template <typename T, int NS>
 struct TcSmem {
   T stage[NS][TC_STAGE];
   double ft[8 * FT_FS];
-  double fs_tout[8 * TO_FS];  // fs [8*FS_FS] then, after a barrier, tout [8*TO_FS]
-  double stile[TC_WARPS][2][ST_SZ];  // PERFIELD variant only
+  double tout[8 * TO_FS];
+  double stile[TC_WARPS][2][ST_SZ];
   unsigned long long bar[NS];
 };
 
@@ -194,11 +184,10 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
   *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-// PERFIELD = true: phase 2 walks the fields one at a time, F_s transposed
-// through a per-warp tile (__syncwarp only), T results exchanged through
-// tout, 2 CTA barriers per element. PERFIELD = false: F_s of all fields
-// goes through an element-wide tile written in phase 1, all 48 DMMAs of an
-// element are independent, 4 CTA barriers per element.
+// Phase 2 walks the fields one at a time: F_s transposed through a
+// per-warp tile (__syncwarp only), T results exchanged through tout, 2 CTA
+// barriers per element. (An all-fields-at-once variant with an element-wide
+// F_s tile and 4 barriers measured 3% slower: profiles/r01_ab_perfield.txt.)
 // SUB = the real Nq. SUB = 8: one element per iteration. SUB = 4 or 2: a
 // "virtual" Nq=8 element packs P^3 real elements (P = 8/SUB) — virtual point
 // (i + SUB a, j + SUB b, k + SUB c) is point (i,j,k) of real element
@@ -207,7 +196,7 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
 // A group of P^3 consecutive elements is the same 8*512 / 9*512 value slab
 // as one Nq=8 element, so the TMA and prefetch code is unchanged; only the
 // thread's own-point offsets inside the slab differ. `ne` counts groups.
-template <typename T, int NS, bool PERFIELD, int SUB>
+template <typename T, int NS, int SUB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
@@ -234,14 +223,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int go = ur * 9 * NPTR + ptr;  // g component 0; components stride NPTR
   const int jo = ur * NPTR + ptr;      // Jinv
   const int ftW = w * FT_PS + gq * 8 + 2 * c;          // own pair in ft
-  const int fsW = fs_at(w, gq, 2 * c);                 // own pair in fs
   const int toR = w * TO_PS + gq * 8 + 2 * c;          // own pair in tout
   const int toW = gq * TO_PS + w * 8 + 2 * c;          // T result (k=g, j=w, i=2c..)
-  int ftR[2], fsR[2];
+  int ftR[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;         // F_t(i=g, j=w, k=c+4t)
-    fsR[t] = fs_at(w, c + 4 * t, gq);                  // F_s(i=g, j=c+4t, k=w)
   }
   // D fragments (D[n*8 + i] = D(i, n)):
   //   R: B[c][g] = D(i=g, n=2c+t);  S and T: A[g][c] = D(g, n=c+4t)
@@ -309,176 +296,92 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     mbar_wait(&bars[st], parity);
 
-    if constexpr (PERFIELD) {
-      // ---- phase 1: point-wise quantities of the thread's two points ------
-      double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
-      {
-        double qv[8][2], gv[9][2];
-#pragma unroll
-        for (int f = 0; f < 8; ++f) ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
-#pragma unroll
-        for (int x = 0; x < 9; ++x) ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
-        double V2[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          double rinv;
-          point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
-#pragma unroll
-          for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
-          V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
-          V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
-          V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            gr[a][s] = gv[a][s];
-            gs[a][s] = gv[3 + a][s];
-          }
-        }
-        sts2(sm.ft + ftW, V2[0], V2[1]);
-#pragma unroll
-        for (int b = 1; b < 8; ++b) {
-          double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
-          if (b <= 3) {
-            f0 += gv[6 + (b - 1)][0] * pP[0];
-            f1 += gv[6 + (b - 1)][1] * pP[1];
-          }
-          sts2(sm.ft + b * FT_FS + ftW, f0, f1);
-        }
-      }
-      __syncthreads();  // ft complete; every stage read of this element is done
-      if (tid == 0 && n + NS < nmine) {
-        fence_proxy_async();
-        issue(n + NS);
-      }
-      // ---- phase 2: per field ----------------------------------------------
-      double acc[8][2];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        double fr[2], fs[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (b == 0) {
-            fr[s] = V0[s];
-            fs[s] = V1[s];
-          } else {
-            fr[s] = V0[s] * sb[b][s];
-            fs[s] = V1[s] * sb[b][s];
-            if (b <= 3) {
-              fr[s] += gr[b - 1][s] * pP[s];
-              fs[s] += gs[b - 1][s] * pP[s];
-            }
-          }
-        }
-        double *stl = sm.stile[w][b & 1];
-        sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
-        __syncwarp();
-        double fsT[2], ftQ[2];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
-          ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
-        }
-        double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          dmma(a0, a1, fr[t], Dr[t]);
-          dmma(a0, a1, Dst[t], fsT[t]);
-          dmma(q0, q1, Dst[t], ftQ[t]);
-        }
-        acc[b][0] = a0;
-        acc[b][1] = a1;
-        sts2(sm.fs_tout + b * TO_FS + toW, q0, q1);
-      }
-      __syncthreads();  // tout complete
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const double2 t = *reinterpret_cast<const double2 *>(sm.fs_tout + b * TO_FS + toR);
-        st_pair(re + qo + b * NPTR, rh[b][0] + jv[0] * (acc[b][0] + t.x),
-                rh[b][1] + jv[1] * (acc[b][1] + t.y));
-      }
-      continue;
-    }
-
-    // ---- phase 1: point-wise work at the thread's two points --------------
-    // F_r of every field stays in registers; F_s and F_t of every field go
-    // to the shared tiles for the transposed readers.
-    double fr[8][2];
+    // ---- phase 1: point-wise quantities of the thread's two points ------
+    double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
     {
       double qv[8][2], gv[9][2];
 #pragma unroll
       for (int f = 0; f < 8; ++f) ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
 #pragma unroll
       for (int x = 0; x < 9; ++x) ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
-      double sb[8][2], V[3][2], pP[2];
+      double V2[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         double rinv;
         point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
 #pragma unroll
         for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
+        V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
+        V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
+        V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-          V[d][s] = gv[3 * d + 0][s] * qv[1][s] + gv[3 * d + 1][s] * qv[2][s] +
-                    gv[3 * d + 2][s] * qv[3][s];
-      }
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        double f[3][2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            f[d][s] = (b == 0) ? V[d][s] : V[d][s] * sb[b][s];
-            if (b >= 1 && b <= 3) f[d][s] += gv[3 * d + (b - 1)][s] * pP[s];
-          }
-          fr[b][s] = f[0][s];
+        for (int a = 0; a < 3; ++a) {
+          gr[a][s] = gv[a][s];
+          gs[a][s] = gv[3 + a][s];
         }
-        sts2(sm.fs_tout + b * FS_FS + fsW, f[1][0], f[1][1]);
-        sts2(sm.ft + b * FT_FS + ftW, f[2][0], f[2][1]);
+      }
+      sts2(sm.ft + ftW, V2[0], V2[1]);
+#pragma unroll
+      for (int b = 1; b < 8; ++b) {
+        double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
+        if (b <= 3) {
+          f0 += gv[6 + (b - 1)][0] * pP[0];
+          f1 += gv[6 + (b - 1)][1] * pP[1];
+        }
+        sts2(sm.ft + b * FT_FS + ftW, f0, f1);
       }
     }
-    __syncthreads();  // (1) fs/ft complete; every stage read of this element done
+    __syncthreads();  // ft complete; every stage read of this element is done
     if (tid == 0 && n + NS < nmine) {
       fence_proxy_async();
       issue(n + NS);
     }
-
-    // ---- phase 2: all 8 fields' contractions, no barrier in between -------
-    double fsT[8][2], ftQ[8][2];
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        fsT[b][t] = sm.fs_tout[b * FS_FS + fsR[t]];
-        ftQ[b][t] = sm.ft[b * FT_FS + ftR[t]];
-      }
-    double acc[8][2], tq[8][2];
+    // ---- phase 2: per field ----------------------------------------------
+    double acc[8][2];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
+      double fr[2], fs[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (b == 0) {
+          fr[s] = V0[s];
+          fs[s] = V1[s];
+        } else {
+          fr[s] = V0[s] * sb[b][s];
+          fs[s] = V1[s] * sb[b][s];
+          if (b <= 3) {
+            fr[s] += gr[b - 1][s] * pP[s];
+            fs[s] += gs[b - 1][s] * pP[s];
+          }
+        }
+      }
+      double *stl = sm.stile[w][b & 1];
+      sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
+      __syncwarp();
+      double fsT[2], ftQ[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
+        ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
+      }
       double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        dmma(a0, a1, fr[b][t], Dr[t]);    // R: A = F_r(n=2c+t, j=g), B = D(i=g, n)
-        dmma(a0, a1, Dst[t], fsT[b][t]);  // S: A = D(j=g, n=c+4t), B = F_s(i=g, j=n)
-        dmma(q0, q1, Dst[t], ftQ[b][t]);  // T: A = D(k=g, n=c+4t), B = F_t(i=g, j=w, k=n)
+        dmma(a0, a1, fr[t], Dr[t]);
+        dmma(a0, a1, Dst[t], fsT[t]);
+        dmma(q0, q1, Dst[t], ftQ[t]);
       }
       acc[b][0] = a0;
       acc[b][1] = a1;
-      tq[b][0] = q0;
-      tq[b][1] = q1;
+      sts2(sm.tout + b * TO_FS + toW, q0, q1);
     }
-    __syncthreads();  // (2) every fs read done: fs storage becomes tout
-#pragma unroll
-    for (int b = 0; b < 8; ++b) sts2(sm.fs_tout + b * TO_FS + toW, tq[b][0], tq[b][1]);
-    __syncthreads();  // (3) tout complete
-
+    __syncthreads();  // tout complete
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const double2 t = *reinterpret_cast<const double2 *>(sm.fs_tout + b * TO_FS + toR);
+      const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
       st_pair(re + qo + b * NPTR, rh[b][0] + jv[0] * (acc[b][0] + t.x),
               rh[b][1] + jv[1] * (acc[b][1] + t.y));
     }
-    __syncthreads();  // (4) tout reads done before the next element's fs writes
   }
 }
 
@@ -486,11 +389,7 @@ template <typename T, int NS, int SUB>
 int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
               const T *D, const T *g, const T *jinv, cudaStream_t stream) {
   const size_t smem = sizeof(TcSmem<T, NS>);
-  static const int perfield = [] {  // A/B knob: LFB_TC_PERFIELD=0|1
-    const char *v = getenv("LFB_TC_PERFIELD");
-    return v ? atoi(v) : 1;
-  }();
-  auto kern = perfield ? volume_tc_kernel<T, NS, true, SUB> : volume_tc_kernel<T, NS, false, SUB>;
+  auto kern = volume_tc_kernel<T, NS, SUB>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
