@@ -214,14 +214,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   // Own points P_s = (i = 2c+s, j = g, k = w): the DMMA C-fragment (row g = j,
   // cols 2c+s = i) of the warp's (i,j)-plane; an adjacent pair in memory.
-  constexpr int P = 8 / SUB, NPTR = SUB * SUB * SUB;
-  static_assert(SUB == 8 || SUB == 4 || SUB == 2, "packing needs SUB | 8, SUB even");
+  // PAD (Nq = 5, 6, 7): one real element zero-padded into the virtual Nq=8
+  // cube; virtual points with a coordinate >= Nq carry zero flux and D is
+  // zero outside [0,Nq)^2, so they neither contribute nor get written.
+  constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
+  static_assert(SUB >= 2 && SUB <= 8, "virtual Nq=8 cube");
+  constexpr int P = PAD ? 1 : 8 / SUB, NPTR = SUB * SUB * SUB;
+  constexpr int SLABQ = PAD ? 8 * NPTR : 8 * TC_NPT;  // values per group: q, rhsq
+  constexpr int SLABG = PAD ? 9 * NPTR : 9 * TC_NPT;  // g
+  constexpr int SLABJ = PAD ? NPTR : TC_NPT;          // Jinv
   // own pair (virtual i = 2c, 2c+1; j = g; k = w) inside the group's slabs
-  const int ur = (2 * c) / SUB + P * (gq / SUB) + P * P * (w / SUB);   // real element
-  const int ptr = ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;  // real point
+  const int ur = PAD ? 0 : (2 * c) / SUB + P * (gq / SUB) + P * P * (w / SUB);  // real element
+  const int ptr = PAD ? (w * SUB + gq) * SUB + 2 * c
+                      : ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;     // real point
   const int qo = ur * 8 * NPTR + ptr;  // q / rhsq field 0; fields stride NPTR
   const int go = ur * 9 * NPTR + ptr;  // g component 0; components stride NPTR
   const int jo = ur * NPTR + ptr;      // Jinv
+  bool vld[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) vld[s] = !PAD || (2 * c + s < SUB && gq < SUB && w < SUB);
   const int ftW = w * FT_PS + gq * 8 + 2 * c;          // own pair in ft
   const int toR = w * TO_PS + gq * 8 + 2 * c;          // own pair in tout
   const int toW = gq * TO_PS + w * 8 + 2 * c;          // T result (k=g, j=w, i=2c..)
@@ -234,8 +245,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   //   R: B[c][g] = D(i=g, n=2c+t);  S and T: A[g][c] = D(g, n=c+4t)
   // (virtual D = blockdiag of the real D for SUB < 8)
   auto Dv = [&](int iv, int nv) -> double {
+    if (PAD) return (iv < SUB && nv < SUB) ? (double)__ldg(D + nv * SUB + iv) : 0.0;
     if (iv / SUB != nv / SUB) return 0.0;
     return (double)__ldg(D + (nv % SUB) * SUB + (iv % SUB));
+  };
+  // 16-byte aligned superset of element e's g slab (PAD: 9 Nq^3 values need
+  // not be a multiple of 16 bytes); returns the copy start and byte count
+  auto gspan = [&](int64_t e, const T *&start, uint32_t &bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(g + e * SLABG);
+    const uintptr_t lo = a & ~(uintptr_t)15;
+    const uintptr_t hi = (a + SLABG * sizeof(T) + 15) & ~(uintptr_t)15;
+    start = reinterpret_cast<const T *>(lo);
+    bytes = (uint32_t)(hi - lo);
+  };
+  auto jspan = [&](int64_t e, const T *&start, uint32_t &bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(jinv + e * SLABJ);
+    const uintptr_t lo = a & ~(uintptr_t)15;
+    const uintptr_t hi = (a + SLABJ * sizeof(T) + 15) & ~(uintptr_t)15;
+    start = reinterpret_cast<const T *>(lo);
+    bytes = (uint32_t)(hi - lo);
   };
   double Dr[2], Dst[2];
 #pragma unroll
@@ -255,9 +283,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   auto issue = [&](int64_t n) {  // element index n (in this CTA's sequence) -> stage n % NS
     const int s = (int)(n % NS);
     const int64_t e = e0 + n * G;
-    mbar_expect_tx(&bars[s], TC_STAGE * sizeof(T));
-    bulk_g2s(sm.stage[s], q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T), &bars[s]);
-    bulk_g2s(sm.stage[s] + 8 * TC_NPT, g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(T), &bars[s]);
+    const T *gs;
+    uint32_t gb;
+    gspan(e, gs, gb);
+    mbar_expect_tx(&bars[s], SLABQ * sizeof(T) + gb);
+    bulk_g2s(sm.stage[s], q + e * SLABQ, SLABQ * sizeof(T), &bars[s]);
+    bulk_g2s(sm.stage[s] + SLABQ, gs, gb, &bars[s]);
   };
   if (tid == 0) {
     for (int64_t n = 0; n < NS && n < nmine; ++n) issue(n);
@@ -268,13 +299,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   auto l2pf = [&](int64_t n) {
     if (tid == 0 && n + NS < nmine) {
       const int64_t e = e0 + (n + NS) * G;
-      prefetch_l2(q + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T));
-      prefetch_l2(g + e * 9 * TC_NPT, 9 * TC_NPT * sizeof(T));
+      const T *gs;
+      uint32_t gb;
+      gspan(e, gs, gb);
+      prefetch_l2(q + e * SLABQ, SLABQ * sizeof(T));
+      prefetch_l2(gs, gb);
     }
     if (tid == 32 && n + 1 < nmine) {
       const int64_t e = e0 + (n + 1) * G;
-      prefetch_l2(rhsq + e * 8 * TC_NPT, 8 * TC_NPT * sizeof(T));
-      prefetch_l2(jinv + e * TC_NPT, TC_NPT * sizeof(T));
+      const T *js;
+      uint32_t jb;
+      jspan(e, js, jb);
+      prefetch_l2(rhsq + e * SLABQ, SLABQ * sizeof(T));
+      prefetch_l2(js, jb);
     }
   };
 
@@ -283,15 +320,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t parity = (uint32_t)((n / NS) & 1);
     const int64_t e = e0 + n * G;
     const T *sq = sm.stage[st];
-    const T *sg = sm.stage[st] + 8 * TC_NPT;
-    T *re = rhsq + e * 8 * TC_NPT;
+    const T *sg = sm.stage[st] + SLABQ +
+                  (PAD ? (reinterpret_cast<uintptr_t>(g + e * SLABG) & 15) / sizeof(T) : 0);
+    T *re = rhsq + e * SLABQ;
 
     // rhsq / Jinv of this element: only needed at write-back, so the latency
     // hides behind the element's compute (and the lines are L2-prefetched)
     double rh[8][2], jv[2];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) ld_pair(re + qo + b * NPTR, rh[b][0], rh[b][1]);
-    ldg_pair(jinv + e * TC_NPT + jo, jv[0], jv[1]);
+    for (int b = 0; b < 8; ++b) {
+      if (PAD) {
+        rh[b][0] = vld[0] ? (double)re[qo + b * NPTR] : 0.0;
+        rh[b][1] = vld[1] ? (double)re[qo + b * NPTR + 1] : 0.0;
+      } else {
+        ld_pair(re + qo + b * NPTR, rh[b][0], rh[b][1]);
+      }
+    }
+    if (PAD) {
+      jv[0] = vld[0] ? (double)jinv[e * SLABJ + jo] : 0.0;
+      jv[1] = vld[1] ? (double)jinv[e * SLABJ + jo + 1] : 0.0;
+    } else {
+      ldg_pair(jinv + e * SLABJ + jo, jv[0], jv[1]);
+    }
     l2pf(n);
 
     mbar_wait(&bars[st], parity);
@@ -301,9 +351,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     {
       double qv[8][2], gv[9][2];
 #pragma unroll
-      for (int f = 0; f < 8; ++f) ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
+      for (int f = 0; f < 8; ++f) {
+        if (PAD) {  // padding points: rho = 1, everything else 0 -> zero flux
+          qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
+          qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
+        } else {
+          ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
+        }
+      }
 #pragma unroll
-      for (int x = 0; x < 9; ++x) ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
+      for (int x = 0; x < 9; ++x) {
+        if (PAD) {
+          gv[x][0] = vld[0] ? (double)sg[go + x * NPTR] : 0.0;
+          gv[x][1] = vld[1] ? (double)sg[go + x * NPTR + 1] : 0.0;
+        } else {
+          ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
+        }
+      }
       double V2[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -379,8 +443,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
-      st_pair(re + qo + b * NPTR, rh[b][0] + jv[0] * (acc[b][0] + t.x),
-              rh[b][1] + jv[1] * (acc[b][1] + t.y));
+      const double o0 = rh[b][0] + jv[0] * (acc[b][0] + t.x);
+      const double o1 = rh[b][1] + jv[1] * (acc[b][1] + t.y);
+      if (PAD) {
+        if (vld[0]) re[qo + b * NPTR] = (T)o0;
+        if (vld[1]) re[qo + b * NPTR + 1] = (T)o1;
+      } else {
+        st_pair(re + qo + b * NPTR, o0, o1);
+      }
     }
   }
 }
@@ -430,11 +500,18 @@ int tail_launch<float>(int nq, int64_t ne, float p0, float R, float gam, const f
 template <typename T, int NS>
 int dispatch_tc(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
                 const T *g, const T *jinv, cudaStream_t s) {
-  const int64_t pe = (int64_t)(8 / nq) * (8 / nq) * (8 / nq);
-  const int64_t groups = ne / pe, done = groups * pe, npt = (int64_t)nq * nq * nq;
+  const bool pad = !(nq == 8 || nq == 4 || nq == 2);
+  const int64_t pe = pad ? 1 : (int64_t)(8 / nq) * (8 / nq) * (8 / nq);
+  // PAD: the last element goes to the tail kernel, so no 16-byte superset
+  // copy of a g / Jinv slab can run past the end of the arrays
+  const int64_t groups = pad ? (ne > 0 ? ne - 1 : 0) : ne / pe;
+  const int64_t done = groups * pe, npt = (int64_t)nq * nq * nq;
   int rc = LFB_OK;
   if (groups > 0) {
     if (nq == 8) rc = launch_tc<T, NS, 8>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+    else if (nq == 7) rc = launch_tc<T, NS, 7>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+    else if (nq == 6) rc = launch_tc<T, NS, 6>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+    else if (nq == 5) rc = launch_tc<T, NS, 5>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
     else if (nq == 4) rc = launch_tc<T, NS, 4>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
     else rc = launch_tc<T, NS, 2>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
   }
@@ -446,7 +523,7 @@ int dispatch_tc(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const
 }  // namespace
 
 bool tc_available(int dtype_bytes, int nq) {
-  return (dtype_bytes == 8 || dtype_bytes == 4) && (nq == 8 || nq == 4 || nq == 2);
+  return (dtype_bytes == 8 || dtype_bytes == 4) && nq >= 2 && nq <= 8 && nq != 3;
 }
 
 // bulk copies need 16-byte aligned q and g element slabs; the paired

@@ -226,11 +226,14 @@ def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device):
     assert max_rel_error(got, want) <= TOL64
 
 
-@pytest.mark.parametrize("nq,ne", [(4, 8 * 300 + 3), (2, 64 * 20 + 17)])
+@pytest.mark.parametrize("nq,ne", [(4, 8 * 300 + 3), (2, 64 * 20 + 17), (5, 201), (6, 302),
+                                   (7, 151)])
 @pytest.mark.parametrize("dtype,tol", [(torch.float64, TOL64), (torch.float32, TOL32)])
 def test_packed_tc_groups_and_tail_against_c_oracle(cuda_device, nq, ne, dtype, tol):
-    """Nq = 4 / 2 run as packed virtual Nq=8 elements (blockdiag D) plus a
-    fused/basic tail; every element against the C oracle."""
+    """Nq = 4 / 2 run as packed virtual Nq=8 elements (blockdiag D), Nq =
+    5..7 as zero-padded ones (odd Nq: unaligned g slabs via 16-byte
+    superset copies), plus a fused/basic tail; every element against the C
+    oracle."""
     st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=8))
     ds = DeviceFieldState.from_field_state(st, dtype=dtype)
     volume_rhs_device(ds, variant="tc")
