@@ -80,8 +80,10 @@ enum {
     LFB_VARIANT_AUTO = 0,    /* best available for (dtype, Nq) */
     LFB_VARIANT_BASIC = 1,   /* column-per-thread, fluxes recomputed per field */
     LFB_VARIANT_FUSED = 2,   /* column-per-thread, fluxes once, register-blocked */
-    LFB_VARIANT_TC = 3       /* Nq=8: TMA-staged, DMMA (fp64 tensor core) contractions;
-                                f32 storage computes in fp64 */
+    LFB_VARIANT_TC = 3,      /* Nq 2,4..8: TMA-staged, DMMA (fp64 tensor core)
+                                contractions on (virtual) Nq=8 planes; f32 storage
+                                computes in fp64 */
+    LFB_VARIANT_LINES = 4    /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -32,8 +32,9 @@ VARIANT_AUTO = 0
 VARIANT_BASIC = 1
 VARIANT_FUSED = 2
 VARIANT_TC = 3
+VARIANT_LINES = 4
 VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
-            "tc": VARIANT_TC}
+            "tc": VARIANT_TC, "lines": VARIANT_LINES}
 
 MAX_NQ = 16
 

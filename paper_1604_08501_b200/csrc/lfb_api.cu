@@ -24,6 +24,11 @@ int volume_tc_f32(int, int64_t, float, float, float, const float *, float *, con
                   const float *, const float *, cudaStream_t);
 bool tc_aligned(int dtype_bytes, const void *q, const void *rhsq, const void *g,
                 const void *jinv);
+int volume_lines_f64(int, int64_t, double, double, double, const double *, double *,
+                     const double *, const double *, const double *, cudaStream_t);
+int volume_lines_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                     const float *, const float *, cudaStream_t);
+bool lines_available(int dtype_bytes, int nq);
 int reverse_axes(int to_batched, int in_bytes, int out_bytes, int ndim, const int64_t *dims,
                  int64_t ne, const void *src, void *dst, cudaStream_t s);
 int make_inputs_device(int nq, int64_t ne, int64_t e_offset, uint64_t seed, int dtype_bytes,
@@ -54,6 +59,7 @@ int resolve(int variant, int bytes, int nq) {
     // measured (profiles/r01_sweep_*.jsonl): the zero-padded tc kernel loses
     // to basic only for fp32 at Nq = 5 (24% of the virtual cube is real)
     if (lfb::tc_available(bytes, nq) && !(bytes == 4 && nq == 5)) return LFB_VARIANT_TC;
+    if (lfb::lines_available(bytes, nq)) return LFB_VARIANT_LINES;
     return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED : LFB_VARIANT_BASIC;
   }
   return variant;
@@ -83,6 +89,9 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
     case LFB_VARIANT_TC:
       if (!lfb::tc_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_tc_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LINES:
+      if (!lfb::lines_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lines_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }
@@ -107,6 +116,9 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
     case LFB_VARIANT_TC:
       if (!lfb::tc_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_tc_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LINES:
+      if (!lfb::lines_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lines_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }
@@ -137,6 +149,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return lfb::fused_available(dtype_bytes, Nq) ? 1 : 0;
     case LFB_VARIANT_TC:
       return lfb::tc_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_LINES:
+      return lfb::lines_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -152,6 +166,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_BASIC: return "basic";
     case LFB_VARIANT_FUSED: return "fused";
     case LFB_VARIANT_TC: return "tc";
+    case LFB_VARIANT_LINES: return "lines";
     default: return "unknown";
   }
 }

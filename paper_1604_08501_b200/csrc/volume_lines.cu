@@ -1,0 +1,247 @@
+// LFB_VARIANT_LINES — large Nq (9..13): the three derivatives as DMMA
+// "line GEMMs" over shared-memory flux tiles.
+//
+// At Nq >= 9 an element no longer fits the tc kernel's scheme (one element's
+// q+g is 99 KB at Nq=9 and 235 KB at Nq=12 in fp64, and the virtual Nq=8
+// planes do not cover it). Here every direction is treated as a GEMM over
+// flattened lines, for one field at a time:
+//   R:  C[i][line(j,k)] = sum_n D(i,n) F_r[n][line]      (lines = Nq^2)
+//   S:  C[j][line(i,k)] = sum_n D(j,n) F_s[n][line]
+//   T:  C[k][line(i,j)] = sum_n D(k,n) F_t[n][line]
+// with m8n8k4 fp64 tiles: M = output position (ceil(Nq/8) tiles, rows >= Nq
+// masked), N = 8 consecutive lines, K = contraction index in steps of 4.
+// Each flux tile is stored line-major with the position fastest, so one
+// B-fragment load is 4 positions x 8 lines. The three results land in three
+// line-major accumulators that the write-back gathers per point.
+//
+// Per element (one CTA of 8 warps per SM, persistent, the next element
+// L2-prefetched with cp.async.bulk.prefetch.L2):
+//   once:      1/rho, p, V_r, V_s, V_t per point -> shared state (q, g read
+//              once from HBM);
+//   per field: fluxes -> 3 tiles | barrier | DMMA line GEMMs -> 3 tiles |
+//              barrier | rhsq += Jinv (R + S + T), coalesced RMW.
+// HBM traffic is the 272 B/pt minimum (q_b and g are re-read per field from
+// L1/L2, not HBM).
+
+#include <stdint.h>
+
+#include "lfb_common.cuh"
+#include "lfb_math.cuh"
+
+namespace lfb {
+namespace {
+
+constexpr int LN_THREADS = 256;
+
+__device__ __forceinline__ void prefetch_l2_lines(const void *p, uint64_t bytes) {
+  // 16-byte aligned superset, split into <= 32 KB requests
+  uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  while (lo < hi) {
+    const uint32_t n = (uint32_t)((hi - lo) > 32768 ? 32768 : (hi - lo));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
+    lo += n;
+  }
+}
+
+__device__ __forceinline__ void dmma_ln(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__device__ __forceinline__ void scalars(double rho, double th, double p0, double Rp0, double gam,
+                                        double &rinv, double &p) {
+  if constexpr (sizeof(T) == 4) {
+    rinv = (double)__frcp_rn((float)rho);
+    p = p0 * (double)exp2f((float)gam * log2f((float)Rp0 * (float)th));
+  } else {
+    rinv = fast_rcp(rho);
+    p = p0 * pos_pow(Rp0 * th, gam);
+  }
+}
+
+template <int NQ>
+struct LinesGeom {
+  static constexpr int NPT = NQ * NQ * NQ;
+  static constexpr int NL = NQ * NQ;                 // lines per direction
+  static constexpr int MT = (NQ + 7) / 8;            // output-position tiles
+  static constexpr int KS = (NQ + 3) / 4;            // k-steps
+  static constexpr int LT = (NL + 7) / 8;            // line tiles
+};
+
+// shared: state[5][NPT] (1/rho, p, V_r, V_s, V_t), flux[3][NPT], acc[3][NPT]
+template <int NQ>
+constexpr size_t lines_smem() {
+  return sizeof(double) * (size_t)(5 + 3 + 3) * LinesGeom<NQ>::NPT;
+}
+
+template <typename T, int NQ>
+__global__ void __launch_bounds__(LN_THREADS, 1)
+    volume_lines_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
+                        T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
+                        const T *__restrict__ jinv) {
+  using Gm = LinesGeom<NQ>;
+  constexpr int NPT = Gm::NPT, NL = Gm::NL, MT = Gm::MT, KS = Gm::KS, LT = Gm::LT;
+  extern __shared__ __align__(16) double lsm[];
+  double *st = lsm;               // [5][NPT]
+  double *fl = lsm + 5 * NPT;     // [3][NPT] line-major: fl[d][line*NQ + pos]
+  double *ac = lsm + 8 * NPT;     // [3][NPT] same layout
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, c = lane & 3;
+  const double Rp0 = R / p0;
+
+  // A fragments: A[g][c] = D(pos = 8 mt + g, n = 4 ks + c), zero outside [0,NQ)
+  double Da[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int pos = 8 * mt + gq, n = 4 * ks + c;
+      Da[mt][ks] = (pos < NQ && n < NQ) ? (double)__ldg(D + n * NQ + pos) : 0.0;
+    }
+
+  for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
+    const T *qe = q + e * 8 * NPT;
+    const T *ge = g + e * 9 * NPT;
+    const T *je = jinv + e * NPT;
+    T *re = rhsq + e * 8 * NPT;
+    const int64_t en = e + gridDim.x;
+    if (en < ne) {
+      if (tid == 0) prefetch_l2_lines(q + en * 8 * NPT, 8ull * NPT * sizeof(T));
+      if (tid == 32) prefetch_l2_lines(g + en * 9 * NPT, 9ull * NPT * sizeof(T));
+      if (tid == 64) prefetch_l2_lines(rhsq + en * 8 * NPT, 8ull * NPT * sizeof(T));
+      if (tid == 96) prefetch_l2_lines(jinv + en * NPT, 1ull * NPT * sizeof(T));
+    }
+
+    // ---- point-wise state (q and g read once from HBM) -------------------
+    for (int pt = tid; pt < NPT; pt += LN_THREADS) {
+      const double rho = (double)qe[pt], u1 = (double)qe[NPT + pt], u2 = (double)qe[2 * NPT + pt],
+                   u3 = (double)qe[3 * NPT + pt], th = (double)qe[4 * NPT + pt];
+      double rinv, p;
+      scalars<T>(rho, th, p0, Rp0, gam, rinv, p);
+      st[pt] = rinv;
+      st[NPT + pt] = p;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        st[(2 + d) * NPT + pt] = (double)ge[(3 * d) * NPT + pt] * u1 +
+                                 (double)ge[(3 * d + 1) * NPT + pt] * u2 +
+                                 (double)ge[(3 * d + 2) * NPT + pt] * u3;
+    }
+    // (the flux pass below reads only the state of its own points)
+
+#pragma unroll 1
+    for (int b = 0; b < 8; ++b) {
+      // ---- fluxes of field b -> line-major tiles -------------------------
+      for (int pt = tid; pt < NPT; pt += LN_THREADS) {
+        const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
+        const double s = (b == 0) ? 1.0 : (double)qe[b * NPT + pt] * st[pt];
+        double f[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          f[d] = st[(2 + d) * NPT + pt] * s;
+          if (b >= 1 && b <= 3) f[d] += (double)ge[(3 * d + (b - 1)) * NPT + pt] * st[NPT + pt];
+        }
+        fl[0 * NPT + (k * NQ + j) * NQ + i] = f[0];  // R line (j,k), position i
+        fl[1 * NPT + (k * NQ + i) * NQ + j] = f[1];  // S line (i,k), position j
+        fl[2 * NPT + (j * NQ + i) * NQ + k] = f[2];  // T line (i,j), position k
+      }
+      __syncthreads();
+
+      // ---- line GEMMs on the fp64 tensor pipe -----------------------------
+      for (int t = warp; t < 3 * LT; t += LN_THREADS / 32) {
+        const int d = t / LT, lt = t % LT;
+        const double *fd = fl + d * NPT;
+        double *ad = ac + d * NPT;
+        const int lineB = 8 * lt + gq;  // B column = line
+        double bv[KS];                  // shared by every output-position tile
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int n = 4 * ks + c;
+          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * NQ + n] : 0.0;
+        }
+        const int l0 = 8 * lt + 2 * c;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) dmma_ln(c0, c1, Da[mt][ks], bv[ks]);
+          const int pos = 8 * mt + gq;
+          if (pos < NQ) {
+            if (l0 < NL) ad[l0 * NQ + pos] = c0;
+            if (l0 + 1 < NL) ad[(l0 + 1) * NQ + pos] = c1;
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- write-back: rhsq += Jinv (R + S + T) ----------------------------
+      for (int pt = tid; pt < NPT; pt += LN_THREADS) {
+        const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
+        const double v = ac[(k * NQ + j) * NQ + i] + ac[NPT + (k * NQ + i) * NQ + j] +
+                         ac[2 * NPT + (j * NQ + i) * NQ + k];
+        T *dst = re + b * NPT + pt;
+        *dst = (T)((double)*dst + (double)je[pt] * v);
+      }
+      // the next field's flux writes touch fl only (last read before the
+      // barrier above); ac is rewritten only after the next barrier
+    }
+    __syncthreads();  // state / fl reuse by the next element
+  }
+}
+
+template <typename T, int NQ>
+int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, const T *D,
+                 const T *g, const T *jinv, cudaStream_t s) {
+  const size_t smem = lines_smem<NQ>();
+  auto kern = volume_lines_kernel<T, NQ>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LFB_ERR_CUDA;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return LFB_ERR_CUDA;
+  const int64_t grid = ne < sms ? ne : sms;
+  if (grid == 0) return LFB_OK;
+  kern<<<(unsigned)grid, LN_THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  LFB_CHECK_LAUNCH();
+  return LFB_OK;
+}
+
+template <typename T>
+int dispatch_lines(int nq, int64_t ne, double p0, double R, double gam, const T *q, T *rhsq,
+                   const T *D, const T *g, const T *jinv, cudaStream_t s) {
+  switch (nq) {
+    case 9: return launch_lines<T, 9>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 10: return launch_lines<T, 10>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 11: return launch_lines<T, 11>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 12: return launch_lines<T, 12>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 13: return launch_lines<T, 13>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    default: return LFB_ERR_BAD_VARIANT;
+  }
+}
+
+}  // namespace
+
+bool lines_available(int dtype_bytes, int nq) {
+  return (dtype_bytes == 8 || dtype_bytes == 4) && nq >= 9 && nq <= 13;
+}
+
+int volume_lines_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                     double *rhsq, const double *D, const double *g, const double *jinv,
+                     cudaStream_t s) {
+  if (!lines_available(8, nq)) return LFB_ERR_BAD_VARIANT;
+  return dispatch_lines<double>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+int volume_lines_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
+                     float *rhsq, const float *D, const float *g, const float *jinv,
+                     cudaStream_t s) {
+  if (!lines_available(4, nq)) return LFB_ERR_BAD_VARIANT;
+  return dispatch_lines<float>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+}
+
+}  // namespace lfb

@@ -29,7 +29,7 @@ SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (2, 130, 3), (3, 2, 3), (3, 33, 4), (
 
 
 def _variants(nbytes, nq):
-    return [v for v in ("basic", "fused", "tc") if _native.variant_available(v, nbytes, nq)]
+    return [v for v in ("basic", "fused", "tc", "lines") if _native.variant_available(v, nbytes, nq)]
 
 
 @pytest.mark.parametrize("nq,ne,seed", SMALL)
@@ -227,16 +227,16 @@ def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device):
 
 
 @pytest.mark.parametrize("nq,ne", [(4, 8 * 300 + 3), (2, 64 * 20 + 17), (5, 201), (6, 302),
-                                   (7, 151)])
+                                   (7, 151), (9, 333), (12, 160), (13, 40)])
 @pytest.mark.parametrize("dtype,tol", [(torch.float64, TOL64), (torch.float32, TOL32)])
 def test_packed_tc_groups_and_tail_against_c_oracle(cuda_device, nq, ne, dtype, tol):
     """Nq = 4 / 2 run as packed virtual Nq=8 elements (blockdiag D), Nq =
     5..7 as zero-padded ones (odd Nq: unaligned g slabs via 16-byte
-    superset copies), plus a fused/basic tail; every element against the C
-    oracle."""
+    superset copies), plus a fused/basic tail; Nq >= 9 through the line-GEMM
+    kernel; every element against the C oracle."""
     st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=8))
     ds = DeviceFieldState.from_field_state(st, dtype=dtype)
-    volume_rhs_device(ds, variant="tc")
+    volume_rhs_device(ds, variant="tc" if nq <= 8 else "lines")
     got = ds.rhsq.to(torch.float64).cpu().numpy()
     q, g, j, d = coracle.to_element_batched(st)
     want = coracle.volume_f64_eb(nq, q, g, j, d, st.constants)
