@@ -31,7 +31,6 @@
 namespace lfb {
 namespace {
 
-constexpr int LN_THREADS = 256;
 
 __device__ __forceinline__ void prefetch_l2_lines(const void *p, uint64_t bytes) {
   // 16-byte aligned superset, split into <= 32 KB requests
@@ -62,6 +61,14 @@ __device__ __forceinline__ void scalars(double rho, double th, double p0, double
   }
 }
 
+// threads per CTA: 16 warps for the large tiles (1 CTA/SM by shared
+// memory), 8 warps x 2 CTAs/SM where two elements' tiles fit
+template <int NQ>
+struct LinesCfg {
+  static constexpr int THREADS = NQ >= 11 ? 512 : 256;
+  static constexpr int MINB = NQ >= 11 ? 1 : 2;
+};
+
 template <int NQ>
 struct LinesGeom {
   static constexpr int NPT = NQ * NQ * NQ;
@@ -69,25 +76,32 @@ struct LinesGeom {
   static constexpr int MT = (NQ + 7) / 8;            // output-position tiles
   static constexpr int KS = (NQ + 3) / 4;            // k-steps
   static constexpr int LT = (NL + 7) / 8;            // line tiles
+  // line stride of the line-major tiles: odd, so the transposed (stride-LS)
+  // flux writes and write-back gathers of a half-warp hit distinct banks
+  static constexpr int LS = NQ | 1;
+  static constexpr int PPT = (NPT + LinesCfg<NQ>::THREADS - 1) / LinesCfg<NQ>::THREADS;
+  static constexpr int TS = NL * LS;                 // one tile
 };
 
-// shared: state[5][NPT] (1/rho, p, V_r, V_s, V_t), flux[3][NPT], acc[3][NPT]
+// shared: state[5][NPT] (1/rho, p, V_r, V_s, V_t), flux[3][TS], acc[3][TS]
 template <int NQ>
 constexpr size_t lines_smem() {
-  return sizeof(double) * (size_t)(5 + 3 + 3) * LinesGeom<NQ>::NPT;
+  return sizeof(double) * ((size_t)5 * LinesGeom<NQ>::NPT + (size_t)6 * LinesGeom<NQ>::TS);
 }
 
 template <typename T, int NQ>
-__global__ void __launch_bounds__(LN_THREADS, 1)
+__global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
     volume_lines_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                         T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                         const T *__restrict__ jinv) {
   using Gm = LinesGeom<NQ>;
+  constexpr int LN_THREADS = LinesCfg<NQ>::THREADS;
   constexpr int NPT = Gm::NPT, NL = Gm::NL, MT = Gm::MT, KS = Gm::KS, LT = Gm::LT;
+  constexpr int LS = Gm::LS, TS = Gm::TS, PPT = Gm::PPT;
   extern __shared__ __align__(16) double lsm[];
-  double *st = lsm;               // [5][NPT]
-  double *fl = lsm + 5 * NPT;     // [3][NPT] line-major: fl[d][line*NQ + pos]
-  double *ac = lsm + 8 * NPT;     // [3][NPT] same layout
+  double *st = lsm;                  // [5][NPT]
+  double *fl = lsm + 5 * NPT;        // [3][TS] line-major: fl[d][line*LS + pos]
+  double *ac = fl + 3 * TS;          // [3][TS] same layout
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, c = lane & 3;
@@ -116,51 +130,80 @@ __global__ void __launch_bounds__(LN_THREADS, 1)
       if (tid == 96) prefetch_l2_lines(jinv + en * NPT, 1ull * NPT * sizeof(T));
     }
 
-    // ---- point-wise state (q and g read once from HBM) -------------------
-    for (int pt = tid; pt < NPT; pt += LN_THREADS) {
-      const double rho = (double)qe[pt], u1 = (double)qe[NPT + pt], u2 = (double)qe[2 * NPT + pt],
-                   u3 = (double)qe[3 * NPT + pt], th = (double)qe[4 * NPT + pt];
-      double rinv, p;
-      scalars<T>(rho, th, p0, Rp0, gam, rinv, p);
-      st[pt] = rinv;
-      st[NPT + pt] = p;
+    // Every per-point loop below is fully unrolled over the thread's PPT
+    // points so its global loads are issued back to back (one L2/HBM round
+    // trip per loop, not per point); rhsq of field b and q_b of field b+1
+    // are loaded before the GEMM phase so their latency hides behind it.
+    double jv[PPT];
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
-        st[(2 + d) * NPT + pt] = (double)ge[(3 * d) * NPT + pt] * u1 +
-                                 (double)ge[(3 * d + 1) * NPT + pt] * u2 +
-                                 (double)ge[(3 * d + 2) * NPT + pt] * u3;
+    for (int m = 0; m < PPT; ++m) {
+      const int pt = tid + m * LN_THREADS;
+      jv[m] = (pt < NPT) ? (double)je[pt] : 0.0;
+    }
+    // ---- point-wise state (q and g read once from HBM) -------------------
+#pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+      const int pt = tid + m * LN_THREADS;
+      if (pt < NPT) {
+        const double rho = (double)qe[pt], u1 = (double)qe[NPT + pt],
+                     u2 = (double)qe[2 * NPT + pt], u3 = (double)qe[3 * NPT + pt],
+                     th = (double)qe[4 * NPT + pt];
+        double rinv, p;
+        scalars<T>(rho, th, p0, Rp0, gam, rinv, p);
+        st[pt] = rinv;
+        st[NPT + pt] = p;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          st[(2 + d) * NPT + pt] = (double)ge[(3 * d) * NPT + pt] * u1 +
+                                   (double)ge[(3 * d + 1) * NPT + pt] * u2 +
+                                   (double)ge[(3 * d + 2) * NPT + pt] * u3;
+      }
     }
     // (the flux pass below reads only the state of its own points)
 
+    double qb[PPT];  // q_b of the field being processed (b >= 1)
 #pragma unroll 1
     for (int b = 0; b < 8; ++b) {
       // ---- fluxes of field b -> line-major tiles -------------------------
-      for (int pt = tid; pt < NPT; pt += LN_THREADS) {
-        const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
-        const double s = (b == 0) ? 1.0 : (double)qe[b * NPT + pt] * st[pt];
-        double f[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          f[d] = st[(2 + d) * NPT + pt] * s;
-          if (b >= 1 && b <= 3) f[d] += (double)ge[(3 * d + (b - 1)) * NPT + pt] * st[NPT + pt];
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+        if (pt < NPT) {
+          const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
+          const double s = (b == 0) ? 1.0 : qb[m] * st[pt];
+          double f[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            f[d] = st[(2 + d) * NPT + pt] * s;
+            if (b >= 1 && b <= 3)
+              f[d] += (double)ge[(3 * d + (b - 1)) * NPT + pt] * st[NPT + pt];
+          }
+          fl[0 * TS + (k * NQ + j) * LS + i] = f[0];  // R line (j,k), position i
+          fl[1 * TS + (k * NQ + i) * LS + j] = f[1];  // S line (i,k), position j
+          fl[2 * TS + (j * NQ + i) * LS + k] = f[2];  // T line (i,j), position k
         }
-        fl[0 * NPT + (k * NQ + j) * NQ + i] = f[0];  // R line (j,k), position i
-        fl[1 * NPT + (k * NQ + i) * NQ + j] = f[1];  // S line (i,k), position j
-        fl[2 * NPT + (j * NQ + i) * NQ + k] = f[2];  // T line (i,j), position k
+      }
+      // loads whose latency the GEMM phase hides
+      double rh[PPT];
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+        rh[m] = (pt < NPT) ? (double)re[b * NPT + pt] : 0.0;
+        if (b < 7) qb[m] = (pt < NPT) ? (double)qe[(b + 1) * NPT + pt] : 0.0;
       }
       __syncthreads();
 
       // ---- line GEMMs on the fp64 tensor pipe -----------------------------
       for (int t = warp; t < 3 * LT; t += LN_THREADS / 32) {
         const int d = t / LT, lt = t % LT;
-        const double *fd = fl + d * NPT;
-        double *ad = ac + d * NPT;
+        const double *fd = fl + d * TS;
+        double *ad = ac + d * TS;
         const int lineB = 8 * lt + gq;  // B column = line
         double bv[KS];                  // shared by every output-position tile
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int n = 4 * ks + c;
-          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * NQ + n] : 0.0;
+          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * LS + n] : 0.0;
         }
         const int l0 = 8 * lt + 2 * c;
 #pragma unroll
@@ -170,20 +213,23 @@ __global__ void __launch_bounds__(LN_THREADS, 1)
           for (int ks = 0; ks < KS; ++ks) dmma_ln(c0, c1, Da[mt][ks], bv[ks]);
           const int pos = 8 * mt + gq;
           if (pos < NQ) {
-            if (l0 < NL) ad[l0 * NQ + pos] = c0;
-            if (l0 + 1 < NL) ad[(l0 + 1) * NQ + pos] = c1;
+            if (l0 < NL) ad[l0 * LS + pos] = c0;
+            if (l0 + 1 < NL) ad[(l0 + 1) * LS + pos] = c1;
           }
         }
       }
       __syncthreads();
 
       // ---- write-back: rhsq += Jinv (R + S + T) ----------------------------
-      for (int pt = tid; pt < NPT; pt += LN_THREADS) {
-        const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
-        const double v = ac[(k * NQ + j) * NQ + i] + ac[NPT + (k * NQ + i) * NQ + j] +
-                         ac[2 * NPT + (j * NQ + i) * NQ + k];
-        T *dst = re + b * NPT + pt;
-        *dst = (T)((double)*dst + (double)je[pt] * v);
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+        if (pt < NPT) {
+          const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
+          const double v = ac[(k * NQ + j) * LS + i] + ac[TS + (k * NQ + i) * LS + j] +
+                           ac[2 * TS + (j * NQ + i) * LS + k];
+          re[b * NPT + pt] = (T)(rh[m] + jv[m] * v);
+        }
       }
       // the next field's flux writes touch fl only (last read before the
       // barrier above); ac is rewritten only after the next barrier
@@ -204,9 +250,15 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return LFB_ERR_CUDA;
-  const int64_t grid = ne < sms ? ne : sms;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LinesCfg<NQ>::THREADS, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return LFB_ERR_LAUNCH;
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, LN_THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  kern<<<(unsigned)grid, LinesCfg<NQ>::THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
