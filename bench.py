@@ -200,6 +200,52 @@ def e2e_run(ds, host, steps: int, warmup: int, chunks: int, variant: str):
     return dt, h2d, d2h, launches
 
 
+def e2e_reference_api(nq: int, ne: int, dev, steps: int, warmup: int):
+    """End to end through the reference's own contract
+    ``reference_volume_term(state)`` (``lf/bench/reference.py:36-70``): the
+    FieldState's f32 C-order arrays (q, g, Jinv; element axis fastest) from
+    pinned host memory to the device as they are, native layout conversion
+    with the cast to fp64 fused, the fp64 kernel on a zeroed rhsq (the
+    increment), native conversion back to the reference's f32 C-order
+    result, device -> host. One stream, every byte every step."""
+    import torch
+    from paper_1604_08501_b200 import (BenchmarkConfig, DeviceFieldState, make_inputs,
+                                       volume_rhs_device)
+    from paper_1604_08501_b200 import _native
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=7))
+    host = {n: torch.from_numpy(getattr(st, n)).pin_memory() for n in ("q", "g", "Jinv")}
+    out_h = torch.empty((nq, nq, nq, 8, ne), dtype=torch.float32).pin_memory()
+    dsrc = {n: torch.empty_like(host[n], device=dev) for n in host}
+    ds = DeviceFieldState.from_field_state(st, dtype=torch.float64, device=dev)
+    out_d = torch.empty((nq, nq, nq, 8, ne), dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    targets = {"q": ds.q, "g": ds.g, "Jinv": ds.Jinv}
+
+    def step():
+        for n in ("q", "g", "Jinv"):
+            dsrc[n].copy_(host[n], non_blocking=True)
+            src = dsrc[n]
+            _native.reverse_axes_ptr(True, 4, 8, src.shape[:-1], ne, src.data_ptr(),
+                                     targets[n].data_ptr(), s.cuda_stream)
+        ds.rhsq.zero_()
+        volume_rhs_device(ds, stream=s)
+        _native.reverse_axes_ptr(False, 8, 4, (nq, nq, nq, 8), ne, ds.rhsq.data_ptr(),
+                                 out_d.data_ptr(), s.cuda_stream)
+        out_h.copy_(out_d, non_blocking=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+    d2h = out_h.numel() * out_h.element_size()
+    return dt, h2d, d2h
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -294,6 +340,7 @@ def run_ours(args) -> None:
 
     # end to end through the public API with host buffers
     e2e = None
+    e2e_ref = None
     if not args.no_e2e:
         host = {n: getattr(ds, n).cpu().pin_memory() for n in ("q", "g", "Jinv", "rhsq")}
         host["out"] = torch.empty_like(host["rhsq"]).pin_memory()
@@ -311,6 +358,14 @@ def run_ours(args) -> None:
                       "buffers (element-batched layout), 2 streams",
                "clocks": e2e_clocks.summary()}
         del host
+        if world == 1 and nq <= 8:
+            sec2, h2d2, d2h2 = e2e_reference_api(nq, ne, dev, e2e_steps, 1)
+            e2e_ref = {"value": pts_total / sec2 / 1e9, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d2, "d2h_bytes_per_step": d2h2,
+                       "ms_per_step": sec2 * 1e3,
+                       "api": "reference_volume_term contract: f32 C-order FieldState "
+                              "arrays (pinned) -> native layout+cast kernels -> fp64 "
+                              "kernel -> f32 C-order increment -> host"}
 
     checksum = global_checksum(ds.rhsq).tolist()
 
@@ -369,7 +424,8 @@ def run_ours(args) -> None:
                                       f"data-path collective",
                        "l2": "working set "
                              f"{alg_bytes / 1e9:.2f} GB/GPU >> 126 MB L2; no flush"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "e2e_reference_api": e2e_ref, "roofline": roofline,
+            "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": args.steps,
             "checksum": {"field_sum": checksum[:8], "field_maxabs": checksum[8:]},
         }

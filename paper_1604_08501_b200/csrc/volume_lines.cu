@@ -141,27 +141,49 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
       jv[m] = (pt < NPT) ? (double)je[pt] : 0.0;
     }
     // ---- point-wise state (q and g read once from HBM) -------------------
+    // two passes so each issues all of its loads before the first use
+    {
+      double rho[PPT], th[PPT];
 #pragma unroll
-    for (int m = 0; m < PPT; ++m) {
-      const int pt = tid + m * LN_THREADS;
-      if (pt < NPT) {
-        const double rho = (double)qe[pt], u1 = (double)qe[NPT + pt],
-                     u2 = (double)qe[2 * NPT + pt], u3 = (double)qe[3 * NPT + pt],
-                     th = (double)qe[4 * NPT + pt];
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+        rho[m] = (pt < NPT) ? (double)qe[pt] : 1.0;
+        th[m] = (pt < NPT) ? (double)qe[4 * NPT + pt] : 1.0;
+      }
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
         double rinv, p;
-        scalars<T>(rho, th, p0, Rp0, gam, rinv, p);
-        st[pt] = rinv;
-        st[NPT + pt] = p;
+        scalars<T>(rho[m], th[m], p0, Rp0, gam, rinv, p);
+        if (pt < NPT) {
+          st[pt] = rinv;
+          st[NPT + pt] = p;
+        }
+      }
+    }
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-          st[(2 + d) * NPT + pt] = (double)ge[(3 * d) * NPT + pt] * u1 +
-                                   (double)ge[(3 * d + 1) * NPT + pt] * u2 +
-                                   (double)ge[(3 * d + 2) * NPT + pt] * u3;
+    for (int d = 0; d < 3; ++d) {
+      double gv[3][PPT], uv[3][PPT];
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gv[a][m] = (pt < NPT) ? (double)ge[(3 * d + a) * NPT + pt] : 0.0;
+          uv[a][m] = (pt < NPT) ? (double)qe[(1 + a) * NPT + pt] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < PPT; ++m) {
+        const int pt = tid + m * LN_THREADS;
+        if (pt < NPT)
+          st[(2 + d) * NPT + pt] = gv[0][m] * uv[0][m] + gv[1][m] * uv[1][m] + gv[2][m] * uv[2][m];
       }
     }
     // (the flux pass below reads only the state of its own points)
 
-    double qb[PPT];  // q_b of the field being processed (b >= 1)
+    double qb[PPT];     // q_b of the field being processed (b >= 1)
+    double gm[3][PPT];  // g(b-1, d) of a momentum field being processed
 #pragma unroll 1
     for (int b = 0; b < 8; ++b) {
       // ---- fluxes of field b -> line-major tiles -------------------------
@@ -175,8 +197,7 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
             f[d] = st[(2 + d) * NPT + pt] * s;
-            if (b >= 1 && b <= 3)
-              f[d] += (double)ge[(3 * d + (b - 1)) * NPT + pt] * st[NPT + pt];
+            if (b >= 1 && b <= 3) f[d] += gm[d][m] * st[NPT + pt];
           }
           fl[0 * TS + (k * NQ + j) * LS + i] = f[0];  // R line (j,k), position i
           fl[1 * TS + (k * NQ + i) * LS + j] = f[1];  // S line (i,k), position j
@@ -190,6 +211,11 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
         const int pt = tid + m * LN_THREADS;
         rh[m] = (pt < NPT) ? (double)re[b * NPT + pt] : 0.0;
         if (b < 7) qb[m] = (pt < NPT) ? (double)qe[(b + 1) * NPT + pt] : 0.0;
+        if (b < 3) {  // the next field is momentum b+1: its g(b, d)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            gm[d][m] = (pt < NPT) ? (double)ge[(3 * d + b) * NPT + pt] : 0.0;
+        }
       }
       __syncthreads();
 
