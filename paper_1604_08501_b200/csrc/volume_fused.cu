@@ -231,14 +231,16 @@ int launch_fused(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
   using C = FusedCfg<T, NQ>;
   constexpr int EPB = C::EPB;
   const size_t smem = C::smem();
-  // tuning knobs for experiments (default: prefetch on, 3 CTAs/SM bound)
+  // tuning knobs for experiments; defaults = the measured best
+  // (profiles/: 4 CTAs/SM bound, no L2 prefetch — prefetching a whole CTA
+  // group ahead overflowed L2 and doubled DRAM reads)
   static const int minb_env = [] {
     const char *v = getenv("LFB_FUSED_MINB");
-    return v ? atoi(v) : 3;
+    return v ? atoi(v) : 4;
   }();
   static const int pf_env = [] {
     const char *v = getenv("LFB_FUSED_PREFETCH");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 0;
   }();
   auto kern = volume_fused_kernel<T, NQ, EPB, true, 3>;
   if (minb_env == 2) kern = pf_env ? volume_fused_kernel<T, NQ, EPB, true, 2>
