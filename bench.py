@@ -200,50 +200,40 @@ def e2e_run(ds, host, steps: int, warmup: int, chunks: int, variant: str):
     return dt, h2d, d2h, launches
 
 
-def e2e_reference_api(nq: int, ne: int, dev, steps: int, warmup: int):
+def e2e_reference_api(nq: int, ne: int, dev, steps: int, warmup: int, seed: int,
+                      chunk: int | None = None):
     """End to end through the reference's own contract
     ``reference_volume_term(state)`` (``lf/bench/reference.py:36-70``): the
-    FieldState's f32 C-order arrays (q, g, Jinv; element axis fastest) from
-    pinned host memory to the device as they are, native layout conversion
-    with the cast to fp64 fused, the fp64 kernel on a zeroed rhsq (the
-    increment), native conversion back to the reference's f32 C-order
-    result, device -> host. One stream, every byte every step."""
+    FieldState's f32 C-order host arrays (q, g, Jinv, D; element axis
+    fastest, page-locked) in, the f32 C-order increment out, fp64 compute —
+    one native call per step (``lfb_volume_host``, INCREMENT mode): chunked
+    2-D H2D copies, on-device layout+cast, the fp64 kernel, conversion back
+    and D2H, overlapped over 3 streams. Every byte crosses PCIe every step.
+    Returns (seconds per step, h2d bytes, d2h bytes, launches per step)."""
     import torch
-    from paper_1604_08501_b200 import (BenchmarkConfig, DeviceFieldState, make_inputs,
-                                       volume_rhs_device)
-    from paper_1604_08501_b200 import _native
-    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=7))
-    host = {n: torch.from_numpy(getattr(st, n)).pin_memory() for n in ("q", "g", "Jinv")}
-    out_h = torch.empty((nq, nq, nq, 8, ne), dtype=torch.float32).pin_memory()
-    dsrc = {n: torch.empty_like(host[n], device=dev) for n in host}
-    ds = DeviceFieldState.from_field_state(st, dtype=torch.float64, device=dev)
-    out_d = torch.empty((nq, nq, nq, 8, ne), dtype=torch.float32, device=dev)
-    s = torch.cuda.current_stream(dev)
-    targets = {"q": ds.q, "g": ds.g, "Jinv": ds.Jinv}
-
-    def step():
-        for n in ("q", "g", "Jinv"):
-            dsrc[n].copy_(host[n], non_blocking=True)
-            src = dsrc[n]
-            _native.reverse_axes_ptr(True, 4, 8, src.shape[:-1], ne, src.data_ptr(),
-                                     targets[n].data_ptr(), s.cuda_stream)
-        ds.rhsq.zero_()
-        volume_rhs_device(ds, stream=s)
-        _native.reverse_axes_ptr(False, 8, 4, (nq, nq, nq, 8), ne, ds.rhsq.data_ptr(),
-                                 out_d.data_ptr(), s.cuda_stream)
-        out_h.copy_(out_d, non_blocking=True)
-
+    from paper_1604_08501_b200 import BenchmarkConfig, FieldState, make_inputs
+    from paper_1604_08501_b200.volume import host_pipeline, volume_host
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=seed))
+    pinned = {n: torch.from_numpy(getattr(st, n)).pin_memory()
+              for n in ("q", "rhsq", "D", "g", "Jinv")}
+    hst = FieldState(*(pinned[n].numpy() for n in ("q", "rhsq", "D", "g", "Jinv")),
+                     st.constants)
+    out_t = torch.empty(st.q.shape, dtype=torch.float32).pin_memory()
+    out = out_t.numpy()
+    pipe = host_pipeline(nq, ne, 4, 8, dev, chunk)
     for _ in range(warmup):
-        step()
+        volume_host(hst, compute_dtype=np.float64, out=out, device=dev, chunk=pipe.chunk)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
-        step()
+        volume_host(hst, compute_dtype=np.float64, out=out, device=dev, chunk=pipe.chunk)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    d2h = out_h.numel() * out_h.element_size()
-    return dt, h2d, d2h
+    h2d = sum(pinned[n].numel() * pinned[n].element_size() for n in ("q", "g", "Jinv", "D"))
+    d2h = out_t.numel() * out_t.element_size()
+    nchunks = -(-ne // pipe.chunk)
+    # per chunk: 4 layout kernels, memset, volume kernel(s); + the D transpose
+    return dt, h2d, d2h, 5 * nchunks + 1, pipe.chunk
 
 
 def run_ours(args) -> None:
@@ -338,43 +328,49 @@ def run_ours(args) -> None:
                 "achieved_tflops": flops_per_point(nq) * pts_rank / (launch_ms * 1e-3) / 1e12,
                 "kernel": kernel_key}
 
-    # end to end through the public API with host buffers
+    # end to end through the reference's entry point with host buffers
     e2e = None
-    e2e_ref = None
+    e2e_eb = None
     if not args.no_e2e:
-        host = {n: getattr(ds, n).cpu().pin_memory() for n in ("q", "g", "Jinv", "rhsq")}
-        host["out"] = torch.empty_like(host["rhsq"]).pin_memory()
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         barrier()
         with ClockSampler(local) as e2e_clocks:
-            sec, h2d, d2h, e2e_launches = e2e_run(ds, host, e2e_steps, 1,
-                                                  args.e2e_chunks, variant)
+            sec, h2d, d2h, e2e_launches, chunk = e2e_reference_api(
+                nq, ne, dev, e2e_steps, 2, 1 + rank, args.e2e_chunk)
         sec = max_over_ranks(sec, device=dev)
         e2e = {"value": pts_total / sec / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": sec * 1e3, "steps": e2e_steps,
-               "chunks": args.e2e_chunks, "launches": e2e_launches,
-               "api": "DeviceFieldState + volume_rhs_device over pinned host "
-                      "buffers (element-batched layout), 2 streams",
+               "launches_per_step": e2e_launches, "chunk_elements": chunk,
+               "api": "reference_volume_term contract (lf/bench/reference.py:36-70) via "
+                      "the native host pipeline lfb_volume_host: the reference's f32 "
+                      "C-order FieldState arrays (page-locked) in, f32 increment out, "
+                      "fp64 compute; H2D + layout + kernel + D2H overlapped over 3 "
+                      "streams",
                "clocks": e2e_clocks.summary()}
-        del host
-        if world == 1 and nq <= 8:
-            sec2, h2d2, d2h2 = e2e_reference_api(nq, ne, dev, e2e_steps, 1)
-            e2e_ref = {"value": pts_total / sec2 / 1e9, "unit": UNIT,
-                       "h2d_bytes_per_step": h2d2, "d2h_bytes_per_step": d2h2,
-                       "ms_per_step": sec2 * 1e3,
-                       "api": "reference_volume_term contract: f32 C-order FieldState "
-                              "arrays (pinned) -> native layout+cast kernels -> fp64 "
-                              "kernel -> f32 C-order increment -> host"}
+        if args.e2e_element_batched:
+            host = {n: getattr(ds, n).cpu().pin_memory() for n in ("q", "g", "Jinv", "rhsq")}
+            host["out"] = torch.empty_like(host["rhsq"]).pin_memory()
+            barrier()
+            sec, h2d, d2h, e2e_launches = e2e_run(ds, host, e2e_steps, 1, 8, variant)
+            sec = max_over_ranks(sec, device=dev)
+            e2e_eb = {"value": pts_total / sec / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "ms_per_step": sec * 1e3, "launches": e2e_launches,
+                      "api": f"DeviceFieldState + volume_rhs_device over pinned host "
+                             f"buffers in the element-batched {args.dtype} layout "
+                             f"(rhsq += v), 8 chunks on 2 streams"}
+            del host
 
     checksum = global_checksum(ds.rhsq).tolist()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and state is None:
-        state = make_inputs(BenchmarkConfig(nq=nq, ne=min(ne, 4096), seed=1))
+        state = make_inputs(BenchmarkConfig(
+            nq=nq, ne=min(ne, args.cpu_sample_per_core * host_cores()), seed=1))
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = host_cores()
-        n = min(ne, max(cores, args.cpu_sample_per_core * cores))
+        n = min(state.ne, max(cores, args.cpu_sample_per_core * cores))
         pool = make_pool(cores, state)
         try:
             cpu_reference_time(state, min(n, cores), cores, pool)  # warm pool
@@ -392,7 +388,7 @@ def run_ours(args) -> None:
         if not args.no_cpu_c:
             from oracle import coracle
             qh, gh, jh, dh = coracle.to_element_batched(
-                make_inputs(BenchmarkConfig(nq=nq, ne=min(ne, 4096), seed=1)))
+                make_inputs(BenchmarkConfig(nq=nq, ne=min(ne, 16384), seed=1)))
             nc = qh.shape[0]
             coracle.volume_f64_eb(nq, qh[:cores], gh[:cores], jh[:cores], dh,
                                   state.constants, nthreads=cores)
@@ -424,7 +420,7 @@ def run_ours(args) -> None:
                                       f"data-path collective",
                        "l2": "working set "
                              f"{alg_bytes / 1e9:.2f} GB/GPU >> 126 MB L2; no flush"},
-            "e2e": e2e, "e2e_reference_api": e2e_ref, "roofline": roofline,
+            "e2e": e2e, "e2e_element_batched": e2e_eb, "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": args.steps,
             "checksum": {"field_sum": checksum[:8], "field_maxabs": checksum[8:]},
@@ -484,10 +480,13 @@ def main(argv=None) -> None:
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--e2e-chunk", type=int, default=None,
+                    help="elements per host-pipeline chunk (default: volume.pipeline_chunk)")
+    ap.add_argument("--e2e-element-batched", action="store_true",
+                    help="also time the fp64 element-batched host-buffer path")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cpu-c", action="store_true")
-    ap.add_argument("--cpu-sample-per-core", type=int, default=48)
+    ap.add_argument("--cpu-sample-per-core", type=int, default=512)
     ap.add_argument("--inputs", choices=("host", "device"), default="host",
                     help="host: make_inputs (bit-identical to the reference); "
                          "device: DeviceFieldState.generate (large configs)")

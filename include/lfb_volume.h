@@ -133,6 +133,33 @@ LFB_API int lfb_make_inputs_device(int Nq, int64_t Ne, int64_t e_offset, uint64_
                                    int dtype_bytes, double p0, double Rgas, void *q,
                                    void *rhsq, void *g, void *Jinv, void *stream);
 
+/* --- host-buffer pipeline (the reference's entry points over HOST arrays) --
+ * Replaces reference_volume_term (lf/bench/reference.py:36-70; mode
+ * LFB_HOST_INCREMENT: v written, fp64 accumulation when compute_bytes = 8)
+ * and interpret_state / volume.f90's rhsq += v (lf/bench/driver.py:54-69;
+ * mode LFB_HOST_ACCUMULATE) for arrays in the reference's HOST layout:
+ * C-order numpy, element axis last — q/rhsq (Nq,Nq,Nq,8,Ne),
+ * g (Nq,Nq,Nq,3,3,Ne), Jinv (Nq,Nq,Nq,Ne), D (Nq,Nq) with D[i][n] = D(i,n).
+ * host_bytes / compute_bytes in {4, 8}: storage of the host arrays / of the
+ * device computation. The pipeline owns device staging for 3 chunks of
+ * `chunk_elements` elements and 3 streams; each chunk is copied in with 2-D
+ * copies, converted, computed, converted back and copied out while the
+ * other chunks are in flight. Host arrays should be page-locked for full
+ * PCIe rate. lfb_volume_host is synchronous (the result is in host memory
+ * on return) and ordered after prior work on `stream`. One pipeline must
+ * not be used by two threads at once. */
+typedef struct lfb_pipeline lfb_pipeline;
+enum { LFB_HOST_INCREMENT = 0, LFB_HOST_ACCUMULATE = 1 };
+LFB_API int lfb_pipeline_create(int Nq, int64_t chunk_elements, int host_bytes,
+                                int compute_bytes, int device, lfb_pipeline **out);
+LFB_API int lfb_pipeline_destroy(lfb_pipeline *p);
+LFB_API int lfb_pipeline_info(const lfb_pipeline *p, int64_t *chunk_elements,
+                              int64_t *device_bytes);
+LFB_API int lfb_volume_host(lfb_pipeline *p, int mode, int64_t Ne, double p0,
+                            double Rgas, double gam, const void *q, const void *D,
+                            const void *g, const void *Jinv, void *rhsq_or_v,
+                            void *stream);
+
 LFB_API const char *lfb_error_string(int code);
 
 /* ABI version: (major << 16) | minor. */

@@ -46,7 +46,12 @@ EXPORTED_SYMBOLS = (
     "lfb_error_string", "lfb_version",
     "lfb_field_state_to_element_batched", "lfb_element_batched_to_field_state",
     "lfb_make_inputs_device",
+    "lfb_pipeline_create", "lfb_pipeline_destroy", "lfb_pipeline_info",
+    "lfb_volume_host",
 )
+
+HOST_INCREMENT = 0
+HOST_ACCUMULATE = 1
 
 _lock = threading.Lock()
 _lib = None
@@ -78,6 +83,14 @@ def _declare(L) -> None:
         fn = getattr(L, name)
         fn.restype = _i
         fn.argtypes = [_i, _i, _i, ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp, _vp]
+    L.lfb_pipeline_create.restype = _i
+    L.lfb_pipeline_create.argtypes = [_i, _i64, _i, _i, _i, ctypes.POINTER(_vp)]
+    L.lfb_pipeline_destroy.restype = _i
+    L.lfb_pipeline_destroy.argtypes = [_vp]
+    L.lfb_pipeline_info.restype = _i
+    L.lfb_pipeline_info.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+    L.lfb_volume_host.restype = _i
+    L.lfb_volume_host.argtypes = [_vp, _i, _i64, _d, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp]
     L.lfb_make_inputs_device.restype = _i
     L.lfb_make_inputs_device.argtypes = [_i, _i64, _i64, ctypes.c_uint64, _i, _d, _d,
                                          _vp, _vp, _vp, _vp, _vp]
@@ -163,3 +176,47 @@ def make_inputs_ptr(nq: int, ne: int, e_offset: int, seed: int, dtype_bytes: int
     check(lib().lfb_make_inputs_device(int(nq), int(ne), int(e_offset), int(seed),
                                        int(dtype_bytes), float(p0), float(R), q, rhsq,
                                        g, jinv, stream), "lfb_make_inputs_device")
+
+
+class HostPipeline:
+    """Owner of one native host-buffer pipeline (``lfb_pipeline_create``):
+    device staging for 3 chunks of ``chunk`` elements and 3 streams. ``run``
+    evaluates the volume term over arrays in the reference's HOST layout
+    (C-order numpy, element axis last) — see include/lfb_volume.h."""
+
+    def __init__(self, nq: int, chunk: int, host_bytes: int, compute_bytes: int,
+                 device: int = -1):
+        L = lib()
+        h = _vp()
+        check(L.lfb_pipeline_create(int(nq), int(chunk), int(host_bytes),
+                                    int(compute_bytes), int(device), ctypes.byref(h)),
+              "lfb_pipeline_create")
+        self._h = h
+        self.nq, self.chunk = int(nq), int(chunk)
+        self.host_bytes, self.compute_bytes = int(host_bytes), int(compute_bytes)
+
+    @property
+    def device_bytes(self) -> int:
+        n = _i64()
+        check(lib().lfb_pipeline_info(self._h, None, ctypes.byref(n)), "lfb_pipeline_info")
+        return int(n.value)
+
+    def run(self, mode: int, ne: int, p0: float, R: float, gam: float, q: int, D: int,
+            g: int, jinv: int, out: int, stream: int = 0) -> None:
+        """Host pointers (ints). Synchronous: the result is in ``out`` on return."""
+        if self._h is None:
+            raise ExecutionError("pipeline is closed")
+        check(lib().lfb_volume_host(self._h, int(mode), int(ne), float(p0), float(R),
+                                    float(gam), q, D, g, jinv, out, stream),
+              "lfb_volume_host")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.lfb_pipeline_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover - GC timing
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

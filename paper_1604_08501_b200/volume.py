@@ -272,19 +272,106 @@ def volume_term(state: FieldState, c: PhysicalConstants | None = None, *,
     return ds.rhsq_logical()
 
 
+#: device staging budget of one pipeline slot (3 slots per pipeline)
+PIPELINE_SLOT_BYTES = 320 << 20
+_PIPELINES: dict = {}
+
+
+def pipeline_chunk(nq: int, ne: int, host_bytes: int, compute_bytes: int,
+                   slot_bytes: int = PIPELINE_SLOT_BYTES) -> int:
+    """Elements per pipeline chunk: the largest power of two whose staging
+    (26 values per point in host and compute dtype) fits ``slot_bytes``, at
+    least 1, at most ``ne``. Nq=8 f32->f64: 2048 elements (8 KB copy rows,
+    the fastest of 1024..16384 in profiles/r01_e2e_chunks.txt)."""
+    per_elem = 26 * nq ** 3 * (host_bytes + compute_bytes)
+    fit = max(1, slot_bytes // per_elem)
+    return max(1, min(int(ne), 1 << (fit.bit_length() - 1)))
+
+
+def host_pipeline(nq: int, ne: int, host_bytes: int, compute_bytes: int,
+                  device=None, chunk: int | None = None) -> "_native.HostPipeline":
+    """A cached native host-buffer pipeline for (device, Nq, dtypes, chunk)."""
+    dev = _device(device)
+    chunk = chunk or pipeline_chunk(nq, ne, host_bytes, compute_bytes)
+    key = (dev.index, nq, host_bytes, compute_bytes, chunk)
+    p = _PIPELINES.get(key)
+    if p is None:
+        if len(_PIPELINES) >= 4:  # bound the cached staging
+            _PIPELINES.pop(next(iter(_PIPELINES))).close()
+        p = _PIPELINES[key] = _native.HostPipeline(nq, chunk, host_bytes, compute_bytes,
+                                                   dev.index)
+    return p
+
+
+def volume_host(state: FieldState, c: PhysicalConstants | None = None, *,
+                accumulate: bool = False, compute_dtype=np.float64, out=None,
+                device=None, chunk: int | None = None, stream=None) -> np.ndarray:
+    """The volume term over HOST arrays in the reference's layout, through
+    the native pipeline (``lfb_volume_host``): chunked 2-D copies, on-device
+    layout conversion, the sm_100a kernel, copies back — all overlapped.
+    ``accumulate=False``: returns the increment v (``reference_volume_term``
+    semantics, rhsq untouched); ``True``: ``state.rhsq += v`` in place.
+    Every array must share one dtype (f32 or f64); ``out`` (increment mode)
+    may be a preallocated C-order array of that dtype, e.g. page-locked."""
+    nq, ne = validate_state(state)
+    arrays = state.arrays()
+    hdt = arrays["q"].dtype
+    for name in ("q", "rhsq", "D", "g", "Jinv"):
+        a = arrays[name]
+        if a.dtype != hdt:
+            raise ExecutionError(f"array {name!r} must be {hdt.name} (one dtype "
+                                 f"for the host pipeline)")
+        if not a.flags.c_contiguous:
+            raise ExecutionError(f"array {name!r} must be C-contiguous")
+    cb = np.dtype(compute_dtype).itemsize
+    if cb not in (4, 8):
+        raise ExecutionError(f"unsupported compute dtype {compute_dtype!r}")
+    c = c or state.constants
+    if accumulate:
+        target = state.rhsq
+    else:
+        target = np.empty(state.q.shape, hdt) if out is None else out
+        if target.shape != state.q.shape or target.dtype != hdt or \
+                not target.flags.c_contiguous:
+            raise ExecutionError("out must be a C-contiguous array shaped like q")
+    if ne == 0:
+        if not accumulate:
+            target[...] = 0
+        return target
+    p = host_pipeline(nq, ne, hdt.itemsize, cb, device, chunk)
+    dev = _device(device)
+    s = stream or torch.cuda.current_stream(dev)
+    p.run(_native.HOST_ACCUMULATE if accumulate else _native.HOST_INCREMENT, ne,
+          c.p0, c.R, c.gamma, state.q.ctypes.data, state.D.ctypes.data,
+          state.g.ctypes.data, state.Jinv.ctypes.data, target.ctypes.data,
+          s.cuda_stream)
+    return target
+
+
 def reference_volume_term(state: FieldState,
                           c: PhysicalConstants | None = None) -> np.ndarray:
     """Drop-in for ``lf/bench/reference.py:36-70``: fp64 accumulation on
-    the GPU, float32 result."""
+    the GPU, float32 result, rhsq untouched. f32 states (what ``make_inputs``
+    builds) take the native host pipeline (``volume_host``)."""
+    validate_state(state)
+    if all(a.dtype == np.float32 and a.flags.c_contiguous
+           for a in state.arrays().values()):
+        return volume_host(state, c, compute_dtype=np.float64)
     return volume_term(state, c, dtype=np.float64).astype(np.float32)
 
 
 def volume_rhs_(state: FieldState, c: PhysicalConstants | None = None, *,
                 dtype=None, device=None, variant="auto") -> np.ndarray:
     """In place ``state.rhsq += v`` (``volume.f90:53-60`` semantics),
-    computed at ``dtype`` (default: the dtype of ``state.rhsq``)."""
+    computed at ``dtype`` (default: the dtype of ``state.rhsq``). Uniform-
+    dtype states with the AUTO variant take the native host pipeline."""
     validate_state(state)
     dt = state.rhsq.dtype if dtype is None else np.dtype(dtype)
+    arrays = state.arrays().values()
+    if variant == "auto" and all(a.dtype == state.rhsq.dtype and a.flags.c_contiguous
+                                 for a in arrays):
+        volume_host(state, c, accumulate=True, compute_dtype=dt, device=device)
+        return state.rhsq
     ds = DeviceFieldState.from_field_state(state, dtype=dt, device=device)
     volume_rhs_device(ds, variant=variant, constants=c or state.constants)
     state.rhsq[...] = ds.rhsq_logical().astype(state.rhsq.dtype, copy=False)
