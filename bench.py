@@ -444,15 +444,17 @@ def run_sweep(args) -> None:
         ne = int(round(1e8 / nq ** 3))
         ds = DeviceFieldState.generate(nq, ne, seed=1, dtype=dt)
         variant = _native.resolve_variant(nbytes, nq)
+        if args.variant != "auto" and _native.variant_available(args.variant, nbytes, nq):
+            variant = args.variant
         for _ in range(args.warmup):
-            volume_rhs_device(ds)
+            volume_rhs_device(ds, variant=variant)
         s = torch.cuda.current_stream()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         steps = max(3, min(args.steps, 50))
         torch.cuda.synchronize()
         a.record(s)
         for _ in range(steps):
-            volume_rhs_device(ds)
+            volume_rhs_device(ds, variant=variant)
         b.record(s)
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / steps

@@ -83,7 +83,9 @@ enum {
     LFB_VARIANT_TC = 3,      /* Nq 2,4..8: TMA-staged, DMMA (fp64 tensor core)
                                 contractions on (virtual) Nq=8 planes; f32 storage
                                 computes in fp64 */
-    LFB_VARIANT_LINES = 4    /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
+    LFB_VARIANT_LINES = 4,   /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
+    LFB_VARIANT_COL = 5      /* Nq 2..12: column owners, FMA in the storage
+                                precision, fluxes through shared line tiles */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -33,8 +33,9 @@ VARIANT_BASIC = 1
 VARIANT_FUSED = 2
 VARIANT_TC = 3
 VARIANT_LINES = 4
+VARIANT_COL = 5
 VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
-            "tc": VARIANT_TC, "lines": VARIANT_LINES}
+            "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL}
 
 MAX_NQ = 16
 

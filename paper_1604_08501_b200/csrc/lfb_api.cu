@@ -29,6 +29,11 @@ int volume_lines_f64(int, int64_t, double, double, double, const double *, doubl
 int volume_lines_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                      const float *, const float *, cudaStream_t);
 bool lines_available(int dtype_bytes, int nq);
+int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
+                   const double *, const double *, const double *, cudaStream_t);
+int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                   const float *, const float *, cudaStream_t);
+bool col_available(int dtype_bytes, int nq);
 int reverse_axes(int to_batched, int in_bytes, int out_bytes, int ndim, const int64_t *dims,
                  int64_t ne, const void *src, void *dst, cudaStream_t s);
 int make_inputs_device(int nq, int64_t ne, int64_t e_offset, uint64_t seed, int dtype_bytes,
@@ -56,9 +61,16 @@ int validate(int nq, int64_t ne, T p0, T R, T gam, const T *q, const T *rhsq,
 
 int resolve(int variant, int bytes, int nq) {
   if (variant == LFB_VARIANT_AUTO) {
-    // measured (profiles/r01_sweep_*.jsonl): the zero-padded tc kernel loses
-    // to basic only for fp32 at Nq = 5 (24% of the virtual cube is real)
-    if (lfb::tc_available(bytes, nq) && !(bytes == 4 && nq == 5)) return LFB_VARIANT_TC;
+    // measured on B200 (profiles/r01_sweep_*.jsonl, profiles/r01_col_sweep_*.jsonl):
+    // col wins where tc pads most of its virtual Nq=8 cube (Nq 5, 6) and
+    // for fp32 above Nq = 8 (FFMA vs the fp64 DMMA line GEMMs); tc keeps
+    // Nq 2, 4, 7, 8; lines keeps fp64 Nq 9, 11, 12
+    if (lfb::col_available(bytes, nq)) {
+      if (nq == 5 || nq == 6) return LFB_VARIANT_COL;
+      if (bytes == 4 && nq >= 9) return LFB_VARIANT_COL;
+      if (bytes == 8 && nq == 10) return LFB_VARIANT_COL;
+    }
+    if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
     if (lfb::lines_available(bytes, nq)) return LFB_VARIANT_LINES;
     return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED : LFB_VARIANT_BASIC;
   }
@@ -77,9 +89,10 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
   if (rc != LFB_OK || Ne == 0) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int v = resolve(variant, 8, Nq);
-  // AUTO never fails on alignment: misaligned arrays take the fused kernel
+  // AUTO never fails on alignment: arrays the TMA kernel cannot take (16-byte
+  // slabs) go to the column kernel, which needs only element alignment
   if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(8, q, rhsq, g, Jinv))
-    v = LFB_VARIANT_FUSED;
+    v = LFB_VARIANT_COL;
   switch (v) {
     case LFB_VARIANT_BASIC:
       return lfb::volume_basic_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -92,6 +105,9 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
     case LFB_VARIANT_LINES:
       if (!lfb::lines_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lines_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_COL:
+      if (!lfb::col_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_col_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }
@@ -106,7 +122,7 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int v = resolve(variant, 4, Nq);
   if (variant == LFB_VARIANT_AUTO && v == LFB_VARIANT_TC && !lfb::tc_aligned(4, q, rhsq, g, Jinv))
-    v = LFB_VARIANT_FUSED;
+    v = LFB_VARIANT_COL;
   switch (v) {
     case LFB_VARIANT_BASIC:
       return lfb::volume_basic_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -119,6 +135,9 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
     case LFB_VARIANT_LINES:
       if (!lfb::lines_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lines_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_COL:
+      if (!lfb::col_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_col_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     default:
       return LFB_ERR_BAD_VARIANT;
   }
@@ -151,6 +170,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return lfb::tc_available(dtype_bytes, Nq) ? 1 : 0;
     case LFB_VARIANT_LINES:
       return lfb::lines_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_COL:
+      return lfb::col_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -167,6 +188,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_FUSED: return "fused";
     case LFB_VARIANT_TC: return "tc";
     case LFB_VARIANT_LINES: return "lines";
+    case LFB_VARIANT_COL: return "col";
     default: return "unknown";
   }
 }

@@ -29,7 +29,8 @@ SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (2, 130, 3), (3, 2, 3), (3, 33, 4), (
 
 
 def _variants(nbytes, nq):
-    return [v for v in ("basic", "fused", "tc", "lines") if _native.variant_available(v, nbytes, nq)]
+    return [v for v in ("basic", "fused", "tc", "lines", "col")
+            if _native.variant_available(v, nbytes, nq)]
 
 
 @pytest.mark.parametrize("nq,ne,seed", SMALL)
@@ -202,12 +203,13 @@ def test_full_size_config2_against_c_oracle(cuda_device, dtype, tol):
     assert err <= tol, err
 
 
-def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device):
+@pytest.mark.parametrize("nq", [8, 7, 2])
+def test_tc_needs_16_byte_alignment_and_auto_falls_back(cuda_device, nq):
     """The TMA/DMMA kernel moves 16-byte pairs; AUTO must still accept any
-    8-byte aligned arrays (it then takes the fused kernel)."""
+    8-byte aligned arrays (it then takes the column kernel)."""
     if not _native.variant_available("tc", 8, 8):
         pytest.skip("no tc kernel")
-    st = make_inputs(BenchmarkConfig(nq=8, ne=5, seed=12))
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=9, seed=12))
     want = O.volume_term_f64_batched(st)
     ds = DeviceFieldState.from_field_state(st, dtype=torch.float64)
     # shift every array by one double inside a bigger buffer
