@@ -51,6 +51,8 @@ int volume_fused_f64(int, int64_t, double, double, double, const double *, doubl
 int volume_fused_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                      const float *, const float *, cudaStream_t);
 bool fused_available(int dtype_bytes, int nq);
+int volume_tc32_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                    const float *, const float *, cudaStream_t);
 
 namespace {
 
@@ -817,6 +819,13 @@ int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float 
                   cudaStream_t s) {
   if (!tc_available(4, nq)) return LFB_ERR_BAD_VARIANT;
   if (!tc_aligned(4, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
+  // fp32 storage: TF32 split-product kernel (volume_tc32.cu); LFB_TC32=0
+  // selects the fp64-DMMA formulation below (A/B knob)
+  static const int tc32_env = [] {
+    const char *v = getenv("LFB_TC32");
+    return v ? atoi(v) : 1;
+  }();
+  if (tc32_env) return volume_tc32_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
   return dispatch_tc<float, 3>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
