@@ -40,6 +40,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "lfb_common.cuh"
 
 namespace lfb {
@@ -145,8 +147,10 @@ struct Smem32 {
   unsigned long long bar[NS];
 };
 
+// NS = 2: 108 KB of shared memory -> two CTAs (16 warps) per SM; NS = 3:
+// one CTA with a deeper ring
 template <int NS, int SUB>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
     volume_tc32_kernel(int64_t ne, float p0, float R, float gam, const float *__restrict__ q,
                        float *__restrict__ rhsq, const float *__restrict__ D,
                        const float *__restrict__ g, const float *__restrict__ jinv) {
@@ -425,22 +429,30 @@ int launch_tc32(int64_t ngroups, float p0, float R, float gam, const float *q, f
 int volume_tc32_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
                     float *rhsq, const float *D, const float *g, const float *jinv,
                     cudaStream_t s) {
-  constexpr int NS = 3;
+  static const int ns_env = [] {
+    const char *v = getenv("LFB_TC32_NS");
+    return v ? atoi(v) : 2;
+  }();
   const bool pad = !(nq == 8 || nq == 4 || nq == 2);
   const int64_t pe = pad ? 1 : (int64_t)(8 / nq) * (8 / nq) * (8 / nq);
   const int64_t groups = pad ? (ne > 0 ? ne - 1 : 0) : ne / pe;
   const int64_t done = groups * pe, npt = (int64_t)nq * nq * nq;
   int rc = LFB_OK;
   if (groups > 0) {
-    switch (nq) {
-      case 8: rc = launch_tc32<NS, 8>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      case 7: rc = launch_tc32<NS, 7>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      case 6: rc = launch_tc32<NS, 6>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      case 5: rc = launch_tc32<NS, 5>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      case 4: rc = launch_tc32<NS, 4>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      case 2: rc = launch_tc32<NS, 2>(groups, p0, R, gam, q, rhsq, D, g, jinv, s); break;
-      default: return LFB_ERR_BAD_VARIANT;
-    }
+    auto run = [&](auto ns) {
+      constexpr int NS = decltype(ns)::value;
+      switch (nq) {
+        case 8: return launch_tc32<NS, 8>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        case 7: return launch_tc32<NS, 7>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        case 6: return launch_tc32<NS, 6>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        case 5: return launch_tc32<NS, 5>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        case 4: return launch_tc32<NS, 4>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        case 2: return launch_tc32<NS, 2>(groups, p0, R, gam, q, rhsq, D, g, jinv, s);
+        default: return (int)LFB_ERR_BAD_VARIANT;
+      }
+    };
+    rc = ns_env == 3 ? run(std::integral_constant<int, 3>{})
+                     : run(std::integral_constant<int, 2>{});
   }
   if (rc != LFB_OK || done == ne) return rc;
   return volume_col_f32(nq, ne - done, p0, R, gam, q + done * 8 * npt, rhsq + done * 8 * npt, D,
