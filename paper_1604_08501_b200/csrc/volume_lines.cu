@@ -24,6 +24,7 @@
 // L1/L2, not HBM).
 
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lfb_common.cuh"
 #include "lfb_math.cuh"
@@ -41,6 +42,39 @@ __device__ __forceinline__ void prefetch_l2_lines(const void *p, uint64_t bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
     lo += n;
   }
+}
+
+// L2 eviction-priority loads: an element's q and g are read in the state
+// pass and re-read (last use) in the per-field passes; keeping the first
+// touch evict_last and the last touch evict_first keeps the re-reads in L2
+// instead of HBM (profiles/r01_lines_l2.txt).
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+  uint64_t p;
+  if (last)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldh(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldh(const float *p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldh_rw(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldh_rw(const float *p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
 }
 
 __device__ __forceinline__ void dmma_ln(double &d0, double &d1, double a, double b) {
@@ -93,7 +127,7 @@ template <typename T, int NQ>
 __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
     volume_lines_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                         T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
-                        const T *__restrict__ jinv) {
+                        const T *__restrict__ jinv, int pf_mode, bool hint) {
   using Gm = LinesGeom<NQ>;
   constexpr int LN_THREADS = LinesCfg<NQ>::THREADS;
   constexpr int NPT = Gm::NPT, NL = Gm::NL, MT = Gm::MT, KS = Gm::KS, LT = Gm::LT;
@@ -106,6 +140,9 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, c = lane & 3;
   const double Rp0 = R / p0;
+  const uint64_t keep = l2_policy(hint), drop = l2_policy(false);
+  auto ld1 = [&](const T *p) -> double { return hint ? (double)ldh(p, keep) : (double)__ldg(p); };
+  auto ld2 = [&](const T *p) -> double { return hint ? (double)ldh(p, drop) : (double)__ldg(p); };
 
   // A fragments: A[g][c] = D(pos = 8 mt + g, n = 4 ks + c), zero outside [0,NQ)
   double Da[MT][KS];
@@ -123,11 +160,11 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
     const T *je = jinv + e * NPT;
     T *re = rhsq + e * 8 * NPT;
     const int64_t en = e + gridDim.x;
-    if (en < ne) {
+    if (en < ne && pf_mode > 0) {
       if (tid == 0) prefetch_l2_lines(q + en * 8 * NPT, 8ull * NPT * sizeof(T));
       if (tid == 32) prefetch_l2_lines(g + en * 9 * NPT, 9ull * NPT * sizeof(T));
-      if (tid == 64) prefetch_l2_lines(rhsq + en * 8 * NPT, 8ull * NPT * sizeof(T));
-      if (tid == 96) prefetch_l2_lines(jinv + en * NPT, 1ull * NPT * sizeof(T));
+      if (pf_mode > 1 && tid == 64) prefetch_l2_lines(rhsq + en * 8 * NPT, 8ull * NPT * sizeof(T));
+      if (pf_mode > 1 && tid == 96) prefetch_l2_lines(jinv + en * NPT, 1ull * NPT * sizeof(T));
     }
 
     // Every per-point loop below is fully unrolled over the thread's PPT
@@ -138,7 +175,7 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
 #pragma unroll
     for (int m = 0; m < PPT; ++m) {
       const int pt = tid + m * LN_THREADS;
-      jv[m] = (pt < NPT) ? (double)je[pt] : 0.0;
+      jv[m] = (pt < NPT) ? ld2(je + pt) : 0.0;
     }
     // ---- point-wise state (q and g read once from HBM) -------------------
     // two passes so each issues all of its loads before the first use
@@ -147,8 +184,8 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
 #pragma unroll
       for (int m = 0; m < PPT; ++m) {
         const int pt = tid + m * LN_THREADS;
-        rho[m] = (pt < NPT) ? (double)qe[pt] : 1.0;
-        th[m] = (pt < NPT) ? (double)qe[4 * NPT + pt] : 1.0;
+        rho[m] = (pt < NPT) ? ld2(qe + pt) : 1.0;
+        th[m] = (pt < NPT) ? ld1(qe + 4 * NPT + pt) : 1.0;
       }
 #pragma unroll
       for (int m = 0; m < PPT; ++m) {
@@ -169,8 +206,8 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
         const int pt = tid + m * LN_THREADS;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          gv[a][m] = (pt < NPT) ? (double)ge[(3 * d + a) * NPT + pt] : 0.0;
-          uv[a][m] = (pt < NPT) ? (double)qe[(1 + a) * NPT + pt] : 0.0;
+          gv[a][m] = (pt < NPT) ? ld1(ge + (3 * d + a) * NPT + pt) : 0.0;
+          uv[a][m] = (pt < NPT) ? ld1(qe + (1 + a) * NPT + pt) : 0.0;
         }
       }
 #pragma unroll
@@ -209,12 +246,12 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
 #pragma unroll
       for (int m = 0; m < PPT; ++m) {
         const int pt = tid + m * LN_THREADS;
-        rh[m] = (pt < NPT) ? (double)re[b * NPT + pt] : 0.0;
-        if (b < 7) qb[m] = (pt < NPT) ? (double)qe[(b + 1) * NPT + pt] : 0.0;
+        rh[m] = (pt < NPT) ? (hint ? (double)ldh_rw(re + b * NPT + pt, drop) : (double)re[b * NPT + pt]) : 0.0;
+        if (b < 7) qb[m] = (pt < NPT) ? ld2(qe + (b + 1) * NPT + pt) : 0.0;
         if (b < 3) {  // the next field is momentum b+1: its g(b, d)
 #pragma unroll
           for (int d = 0; d < 3; ++d)
-            gm[d][m] = (pt < NPT) ? (double)ge[(3 * d + b) * NPT + pt] : 0.0;
+            gm[d][m] = (pt < NPT) ? ld2(ge + (3 * d + b) * NPT + pt) : 0.0;
         }
       }
       __syncthreads();
@@ -284,7 +321,22 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, LinesCfg<NQ>::THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  // L2 prefetch of the next element: 0 none, 1 q + g, 2 q + g + rhsq + Jinv.
+  // Default 0: a whole next element per CTA (360 KB at Nq=12 fp64, 53 MB
+  // chip-wide) thrashes L2 against the per-field re-reads (+42 % DRAM
+  // reads, -15 % speed); without it DRAM traffic is exactly algorithmic
+  // (profiles/r01_lines_l2.txt)
+  static const int pf_env = [] {
+    const char *v = getenv("LFB_LINES_PF");
+    return v ? atoi(v) : 0;
+  }();
+  // L2 eviction hints on the q / g / rhsq loads (1) or plain loads (0)
+  static const int hint_env = [] {
+    const char *v = getenv("LFB_LINES_HINT");
+    return v ? atoi(v) : 1;
+  }();
+  kern<<<(unsigned)grid, LinesCfg<NQ>::THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv,
+                                                           pf_env, hint_env != 0);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
