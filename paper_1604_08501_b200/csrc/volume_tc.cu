@@ -715,6 +715,259 @@ int launch_tc_lean(int64_t ngroups, double p0, double R, double gam, const T *q,
   return LFB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// QSTAGE schedule (fp64): two CTAs (16 warps) per SM so the kernel stays
+// HBM-bound when the SM clock drops under the power cap (the 1-CTA schedule
+// is 8 % slower at ~1.8 GHz than at 1.965 GHz). Only q goes through a TMA
+// stage (32 KB); g is read straight from global memory into registers (its
+// lines are L2-prefetched one element ahead), rhsq and Jinv at write-back.
+// After phase 1 the dead q stage holds the per-warp S tiles; the next
+// element's q is copied in as soon as phase 2 is done, behind the
+// write-back. Shared memory 104 KB, <= 128 registers.
+template <typename T>
+struct TcSmemQ {
+  T qstage[8 * TC_NPT];
+  double ft[8 * FT_FS];
+  double tout[8 * TO_FS];
+  unsigned long long bar;
+};
+static_assert(TC_WARPS * 2 * ST_SZ * sizeof(double) <= 8 * TC_NPT * sizeof(double),
+              "S tiles fit in the dead q stage");
+
+template <typename T, int SUB>
+__global__ void __launch_bounds__(TC_THREADS, 2)
+    volume_tc_q_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
+                       T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
+                       const T *__restrict__ jinv) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TcSmemQ<T> &sm = *reinterpret_cast<TcSmemQ<T> *>(smem_raw);
+  double *const stiles = reinterpret_cast<double *>(sm.qstage);  // [w][2][ST_SZ] after phase 1
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, c = lane & 3;
+  const int64_t G = gridDim.x;
+  const int64_t e0 = blockIdx.x;
+  const int64_t nmine = (e0 < ne) ? (ne - 1 - e0) / G + 1 : 0;
+  const double Rp0 = R / p0;
+
+  constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
+  static_assert(SUB >= 2 && SUB <= 8, "virtual Nq=8 cube");
+  constexpr int P = PAD ? 1 : 8 / SUB, NPTR = SUB * SUB * SUB;
+  constexpr int SLABQ = PAD ? 8 * NPTR : 8 * TC_NPT;
+  constexpr int SLABG = PAD ? 9 * NPTR : 9 * TC_NPT;
+  constexpr int SLABJ = PAD ? NPTR : TC_NPT;
+  const int ur = PAD ? 0 : (2 * c) / SUB + P * (gq / SUB) + P * P * (w / SUB);
+  const int ptr = PAD ? (w * SUB + gq) * SUB + 2 * c
+                      : ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;
+  const int qo = ur * 8 * NPTR + ptr;
+  const int go = ur * 9 * NPTR + ptr;
+  const int jo = ur * NPTR + ptr;
+  bool vld[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) vld[s] = !PAD || (2 * c + s < SUB && gq < SUB && w < SUB);
+  const int ftW = w * FT_PS + gq * 8 + 2 * c;
+  const int toR = w * TO_PS + gq * 8 + 2 * c;
+  const int toW = gq * TO_PS + w * 8 + 2 * c;
+  int ftR[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;
+  auto Dv = [&](int iv, int nv) -> double {
+    if (PAD) return (iv < SUB && nv < SUB) ? (double)__ldg(D + nv * SUB + iv) : 0.0;
+    if (iv / SUB != nv / SUB) return 0.0;
+    return (double)__ldg(D + (nv % SUB) * SUB + (iv % SUB));
+  };
+  double Dr[2], Dst[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    Dr[t] = Dv(gq, 2 * c + t);
+    Dst[t] = Dv(gq, c + 4 * t);
+  }
+  auto span16 = [](const T *p, size_t n, const T *&start, uint32_t &bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t lo = a & ~(uintptr_t)15;
+    const uintptr_t hi = (a + n * sizeof(T) + 15) & ~(uintptr_t)15;
+    start = reinterpret_cast<const T *>(lo);
+    bytes = (uint32_t)(hi - lo);
+  };
+
+  uint64_t *bar = reinterpret_cast<uint64_t *>(&sm.bar);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t n) {
+    const int64_t e = e0 + n * G;
+    mbar_expect_tx(bar, SLABQ * sizeof(T));
+    bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
+  };
+  if (tid == 0 && nmine > 0) issue(0);
+
+  for (int64_t n = 0; n < nmine; ++n) {
+    const int64_t e = e0 + n * G;
+    if (n + 1 < nmine) {  // L2 prefetch of the next element
+      const int64_t en = e + G;
+      const T *sp;
+      uint32_t sb_;
+      if (tid == 0) {
+        prefetch_l2(q + en * SLABQ, SLABQ * sizeof(T));
+      } else if (tid == 32) {
+        span16(g + en * SLABG, SLABG, sp, sb_);
+        prefetch_l2(sp, sb_);
+      } else if (tid == 64) {
+        prefetch_l2(rhsq + en * SLABQ, SLABQ * sizeof(T));
+        span16(jinv + en * SLABJ, SLABJ, sp, sb_);
+        prefetch_l2(sp, sb_);
+      }
+    }
+    const T *ge = g + e * SLABG;
+    T *re = rhsq + e * SLABQ;
+
+    // ---- phase 1: g from global (issued before the q wait), q from the stage
+    double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
+    {
+      double gv[9][2];
+#pragma unroll
+      for (int x = 0; x < 9; ++x) {
+        if (PAD) {
+          gv[x][0] = vld[0] ? (double)__ldg(ge + go + x * NPTR) : 0.0;
+          gv[x][1] = vld[1] ? (double)__ldg(ge + go + x * NPTR + 1) : 0.0;
+        } else {
+          ldg_pair(ge + go + x * NPTR, gv[x][0], gv[x][1]);
+        }
+      }
+      mbar_wait(bar, (uint32_t)(n & 1));
+      const T *sq = sm.qstage;
+      double qv[8][2];
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        if (PAD) {
+          qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
+          qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
+        } else {
+          ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
+        }
+      }
+      double V2[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        double rinv;
+        point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
+#pragma unroll
+        for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
+        V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
+        V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
+        V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gr[a][s] = gv[a][s];
+          gs[a][s] = gv[3 + a][s];
+        }
+      }
+      sts2(sm.ft + ftW, V2[0], V2[1]);
+#pragma unroll
+      for (int b = 1; b < 8; ++b) {
+        double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
+        if (b <= 3) {
+          f0 += gv[6 + (b - 1)][0] * pP[0];
+          f1 += gv[6 + (b - 1)][1] * pP[1];
+        }
+        sts2(sm.ft + b * FT_FS + ftW, f0, f1);
+      }
+    }
+    __syncthreads();  // ft complete; the q stage is dead -> S tiles
+    // ---- phase 2 (as in the 1-CTA kernel) -----------------------------------
+    double acc[8][2];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      double fr[2], fs[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (b == 0) {
+          fr[s] = V0[s];
+          fs[s] = V1[s];
+        } else {
+          fr[s] = V0[s] * sb[b][s];
+          fs[s] = V1[s] * sb[b][s];
+          if (b <= 3) {
+            fr[s] += gr[b - 1][s] * pP[s];
+            fs[s] += gs[b - 1][s] * pP[s];
+          }
+        }
+      }
+      double *stl = stiles + (w * 2 + (b & 1)) * ST_SZ;
+      sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
+      __syncwarp();
+      double fsT[2], ftQ[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
+        ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
+      }
+      double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        dmma(a0, a1, fr[t], Dr[t]);
+        dmma(a0, a1, Dst[t], fsT[t]);
+        dmma(q0, q1, Dst[t], ftQ[t]);
+      }
+      acc[b][0] = a0;
+      acc[b][1] = a1;
+      sts2(sm.tout + b * TO_FS + toW, q0, q1);
+    }
+    __syncthreads();  // tout complete; S tiles dead -> the q stage may be refilled
+    if (tid == 0 && n + 1 < nmine) {
+      fence_proxy_async();
+      issue(n + 1);
+    }
+    // ---- write-back (rhsq, Jinv read here: L2-prefetched) -------------------
+    double jv[2];
+    if (PAD) {
+      jv[0] = vld[0] ? (double)__ldg(jinv + e * SLABJ + jo) : 0.0;
+      jv[1] = vld[1] ? (double)__ldg(jinv + e * SLABJ + jo + 1) : 0.0;
+    } else {
+      ldg_pair(jinv + e * SLABJ + jo, jv[0], jv[1]);
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
+      if (PAD) {
+        if (vld[0]) re[qo + b * NPTR] = (T)((double)re[qo + b * NPTR] + jv[0] * (acc[b][0] + t.x));
+        if (vld[1])
+          re[qo + b * NPTR + 1] = (T)((double)re[qo + b * NPTR + 1] + jv[1] * (acc[b][1] + t.y));
+      } else {
+        double r0, r1;
+        ld_pair(re + qo + b * NPTR, r0, r1);
+        st_pair(re + qo + b * NPTR, r0 + jv[0] * (acc[b][0] + t.x), r1 + jv[1] * (acc[b][1] + t.y));
+      }
+    }
+  }
+}
+
+template <typename T, int SUB>
+int launch_tc_q(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
+                const T *D, const T *g, const T *jinv, cudaStream_t stream) {
+  const size_t smem = sizeof(TcSmemQ<T>);
+  auto kern = volume_tc_q_kernel<T, SUB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LFB_ERR_CUDA;
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem) !=
+          cudaSuccess)
+    return LFB_ERR_CUDA;
+  if (per_sm < 1) return LFB_ERR_LAUNCH;
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t grid = ngroups < slots ? ngroups : slots;
+  if (grid == 0) return LFB_OK;
+  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
+  LFB_CHECK_LAUNCH();
+  return LFB_OK;
+}
+
 template <typename T, int NS, int SUB>
 int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
               const T *D, const T *g, const T *jinv, cudaStream_t stream) {
@@ -727,6 +980,13 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
     return v ? atoi(v) : -1;
   }();
   constexpr bool PAD_ = !(SUB == 8 || SUB == 4 || SUB == 2);
+  // LFB_TC_QSTAGE=1: the 2-CTA q-staged schedule (fp64 A/B knob)
+  static const int qs_env = [] {
+    const char *v = getenv("LFB_TC_QSTAGE");
+    return v ? atoi(v) : 0;
+  }();
+  if (sizeof(T) == 8 && qs_env > 0)
+    return launch_tc_q<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   const bool lean = lean_env >= 0 ? lean_env != 0 : (PAD_ || (sizeof(T) == 4 && SUB == 8));
   if (lean) return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   const size_t smem = sizeof(TcSmem<T, NS>);
