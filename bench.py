@@ -236,6 +236,46 @@ def e2e_reference_api(nq: int, ne: int, dev, steps: int, warmup: int, seed: int,
     return dt, h2d, d2h, 5 * nchunks + 1, pipe.chunk
 
 
+def emitted_reference_gpu(nq: int, ne: int, dev, steps: int = 20):
+    """The reference's emitted level-8 kernel (tests/golden/emitted/, the
+    text of lf/codegen.py:emit_source) compiled unchanged by NVRTC for
+    sm_100a (paper_1604_08501_b200.emitted) and timed on this GPU on the
+    same workload at fp32, against the hand-written fp32 kernel."""
+    import torch
+    from paper_1604_08501_b200 import DeviceFieldState, volume_rhs_device
+    from paper_1604_08501_b200.emitted import EmittedKernel
+    path = ROOT / "tests" / "golden" / "emitted" / f"level8_nq{nq}.cl"
+    if not path.exists():
+        return None
+    ds = DeviceFieldState.generate(nq, ne, seed=1, dtype=torch.float32, device=dev)
+    k = EmittedKernel.from_file(path)
+    b = k.bind(ds)
+    s = torch.cuda.current_stream(dev)
+
+    def t(fn):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(steps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    ms_ref = t(lambda: k.launch(b, s))
+    ms_ours = t(lambda: volume_rhs_device(ds, stream=s))
+    k.close()
+    pts = nq ** 3 * ne
+    return {"value": pts / (ms_ref * 1e-3) / 1e9, "unit": UNIT, "dtype": "f32",
+            "ms_per_launch": ms_ref, "ours_f32_ms_per_launch": ms_ours,
+            "speedup_ours_f32": ms_ref / ms_ours,
+            "kernel": "reference level-8 emitted kernel fused_r_s (lf/codegen.py:443-460 "
+                      "output, tests/golden/emitted/level8_nq8.cl) compiled unchanged by "
+                      "NVRTC for sm_100a, launch Ne x (8x8) as emitted"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -364,6 +404,12 @@ def run_ours(args) -> None:
 
     checksum = global_checksum(ds.rhsq).tolist()
 
+    # the reference's own best kernel (emitted level 8, compiled unchanged
+    # for sm_100a) on the same GPU — fp32, its only precision
+    emitted = None
+    if rank == 0 and world == 1 and not args.no_emitted and nq == 8:
+        emitted = emitted_reference_gpu(nq, ne, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and state is None:
         state = make_inputs(BenchmarkConfig(
@@ -421,6 +467,7 @@ def run_ours(args) -> None:
                        "l2": "working set "
                              f"{alg_bytes / 1e9:.2f} GB/GPU >> 126 MB L2; no flush"},
             "e2e": e2e, "e2e_element_batched": e2e_eb, "roofline": roofline,
+            "reference_emitted_gpu": emitted,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": args.steps,
             "checksum": {"field_sum": checksum[:8], "field_maxabs": checksum[8:]},
@@ -487,6 +534,8 @@ def main(argv=None) -> None:
     ap.add_argument("--e2e-element-batched", action="store_true",
                     help="also time the fp64 element-batched host-buffer path")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-emitted", action="store_true",
+                    help="skip timing the reference's emitted level-8 kernel on the GPU")
     ap.add_argument("--no-cpu-c", action="store_true")
     ap.add_argument("--cpu-sample-per-core", type=int, default=512)
     ap.add_argument("--inputs", choices=("host", "device"), default="host",

@@ -63,7 +63,8 @@ enum {
     LFB_ERR_CUDA = 6,          /* other CUDA runtime failure */
     LFB_ERR_BAD_CONSTANTS = 7, /* not (p0 > 0, R > 0, gam > 1) */
     LFB_ERR_BAD_VARIANT = 8,   /* unknown kernel variant id */
-    LFB_ERR_ALLOC = 9          /* device/host staging allocation failed */
+    LFB_ERR_ALLOC = 9,         /* device/host staging allocation failed */
+    LFB_ERR_EMIT_COMPILE = 10  /* emitted-kernel source failed to compile (lfb_emitted.h) */
 };
 
 #define LFB_MAX_NQ 16

@@ -205,6 +205,7 @@ const char *lfb_error_string(int code) {
     case LFB_ERR_BAD_CONSTANTS: return "need p0 > 0, R > 0, gamma > 1";
     case LFB_ERR_BAD_VARIANT: return "unknown or unavailable kernel variant";
     case LFB_ERR_ALLOC: return "staging allocation failed";
+    case LFB_ERR_EMIT_COMPILE: return "emitted kernel source failed to compile (see the NVRTC log)";
     default: return "unknown error";
   }
 }
