@@ -2,10 +2,8 @@ set -x
 T=${1:-san}
 mkdir -p gpurun_out
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest.txt 2>&1
-timeout 300 python bench.py --dtype f32 --no-e2e --no-cpu > gpurun_out/${T}_bench_f32.txt 2>&1
-timeout 300 python bench.py --no-e2e --no-cpu > gpurun_out/${T}_bench_f64.txt 2>&1
 for tool in racecheck synccheck memcheck initcheck; do
-  timeout 900 compute-sanitizer --tool $tool --kernel-name kns=lfb python tools/sanitize_run.py > gpurun_out/${T}_sanitizer_${tool}.txt 2>&1
+  timeout 1200 compute-sanitizer --tool $tool --kernel-name kns=lfb python tools/sanitize_run.py > gpurun_out/${T}_sanitizer_${tool}.txt 2>&1
+  LFB_TC_LEAN=1 LFB_TC32=0 timeout 600 compute-sanitizer --tool $tool --kernel-name kns=lfb python tools/sanitize_run.py > gpurun_out/${T}_sanitizer_${tool}_alt.txt 2>&1
+  timeout 600 compute-sanitizer --tool $tool python tools/sanitize_run.py emitted > gpurun_out/${T}_sanitizer_${tool}_emitted.txt 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_tc -s 3 -c 1 -o gpurun_out/${T}_tc32 python bench.py --dtype f32 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_full.log 2>&1
