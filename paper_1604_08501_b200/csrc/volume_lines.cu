@@ -103,39 +103,55 @@ struct LinesCfg {
   static constexpr int MINB = NQ >= 11 ? 1 : 2;
 };
 
-template <int NQ>
+constexpr int stride_mod16(int nq, int r1, int r2) {
+  int l = nq;
+  while (l % 16 != r1 && l % 16 != r2) ++l;
+  return l;
+}
+
+// MODE 0: one odd line stride for every tile. MODE 1 (default): per tile
+// kind, chosen for its fragment access (64-bit accesses are served 16 lanes
+// = 16 double slots at a time; conflict-free iff addr mod 16 distinct):
+//   flux tiles, read as B fragments (line 8lt+g, pos 4ks+c; g, c < 4 per
+//     half-warp): stride = 4 or 12 mod 16 -> {12g + c} distinct;
+//   accumulator tiles, written as C fragments (lines 8lt+2c(+1), pos 8mt+g):
+//     stride = 2 mod 16 -> {4c + g} distinct.
+// (profiles/r01_lines_banks.txt: MODE 0 makes a third of the shared
+// wavefronts bank-conflict replays, but MODE 1 is slower — see launch_lines.)
+template <int NQ, int MODE>
 struct LinesGeom {
   static constexpr int NPT = NQ * NQ * NQ;
   static constexpr int NL = NQ * NQ;                 // lines per direction
   static constexpr int MT = (NQ + 7) / 8;            // output-position tiles
   static constexpr int KS = (NQ + 3) / 4;            // k-steps
   static constexpr int LT = (NL + 7) / 8;            // line tiles
-  // line stride of the line-major tiles: odd, so the transposed (stride-LS)
-  // flux writes and write-back gathers of a half-warp hit distinct banks
-  static constexpr int LS = NQ | 1;
+  static constexpr int LSF = MODE == 0 ? (NQ | 1) : stride_mod16(NQ, 4, 12);
+  static constexpr int LSA = MODE == 0 ? (NQ | 1) : stride_mod16(NQ, 2, 2);
   static constexpr int PPT = (NPT + LinesCfg<NQ>::THREADS - 1) / LinesCfg<NQ>::THREADS;
-  static constexpr int TS = NL * LS;                 // one tile
+  static constexpr int TSF = NL * LSF;               // one flux tile
+  static constexpr int TSA = NL * LSA;               // one accumulator tile
 };
 
-// shared: state[5][NPT] (1/rho, p, V_r, V_s, V_t), flux[3][TS], acc[3][TS]
-template <int NQ>
+// shared: state[5][NPT] (1/rho, p, V_r, V_s, V_t), flux[3][TSF], acc[3][TSA]
+template <int NQ, int MODE>
 constexpr size_t lines_smem() {
-  return sizeof(double) * ((size_t)5 * LinesGeom<NQ>::NPT + (size_t)6 * LinesGeom<NQ>::TS);
+  using Gm = LinesGeom<NQ, MODE>;
+  return sizeof(double) * ((size_t)5 * Gm::NPT + (size_t)3 * (Gm::TSF + Gm::TSA));
 }
 
-template <typename T, int NQ>
+template <typename T, int NQ, int MODE>
 __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
     volume_lines_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                         T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                         const T *__restrict__ jinv, int pf_mode, bool hint) {
-  using Gm = LinesGeom<NQ>;
+  using Gm = LinesGeom<NQ, MODE>;
   constexpr int LN_THREADS = LinesCfg<NQ>::THREADS;
   constexpr int NPT = Gm::NPT, NL = Gm::NL, MT = Gm::MT, KS = Gm::KS, LT = Gm::LT;
-  constexpr int LS = Gm::LS, TS = Gm::TS, PPT = Gm::PPT;
+  constexpr int LSF = Gm::LSF, LSA = Gm::LSA, TSF = Gm::TSF, TSA = Gm::TSA, PPT = Gm::PPT;
   extern __shared__ __align__(16) double lsm[];
   double *st = lsm;                  // [5][NPT]
-  double *fl = lsm + 5 * NPT;        // [3][TS] line-major: fl[d][line*LS + pos]
-  double *ac = fl + 3 * TS;          // [3][TS] same layout
+  double *fl = lsm + 5 * NPT;        // [3][TSF] line-major: fl[d][line*LSF + pos]
+  double *ac = fl + 3 * TSF;         // [3][TSA] line-major: ac[d][line*LSA + pos]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, c = lane & 3;
@@ -236,9 +252,9 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
             f[d] = st[(2 + d) * NPT + pt] * s;
             if (b >= 1 && b <= 3) f[d] += gm[d][m] * st[NPT + pt];
           }
-          fl[0 * TS + (k * NQ + j) * LS + i] = f[0];  // R line (j,k), position i
-          fl[1 * TS + (k * NQ + i) * LS + j] = f[1];  // S line (i,k), position j
-          fl[2 * TS + (j * NQ + i) * LS + k] = f[2];  // T line (i,j), position k
+          fl[0 * TSF + (k * NQ + j) * LSF + i] = f[0];  // R line (j,k), position i
+          fl[1 * TSF + (k * NQ + i) * LSF + j] = f[1];  // S line (i,k), position j
+          fl[2 * TSF + (j * NQ + i) * LSF + k] = f[2];  // T line (i,j), position k
         }
       }
       // loads whose latency the GEMM phase hides
@@ -259,14 +275,14 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
       // ---- line GEMMs on the fp64 tensor pipe -----------------------------
       for (int t = warp; t < 3 * LT; t += LN_THREADS / 32) {
         const int d = t / LT, lt = t % LT;
-        const double *fd = fl + d * TS;
-        double *ad = ac + d * TS;
+        const double *fd = fl + d * TSF;
+        double *ad = ac + d * TSA;
         const int lineB = 8 * lt + gq;  // B column = line
         double bv[KS];                  // shared by every output-position tile
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int n = 4 * ks + c;
-          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * LS + n] : 0.0;
+          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * LSF + n] : 0.0;
         }
         const int l0 = 8 * lt + 2 * c;
 #pragma unroll
@@ -276,8 +292,8 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
           for (int ks = 0; ks < KS; ++ks) dmma_ln(c0, c1, Da[mt][ks], bv[ks]);
           const int pos = 8 * mt + gq;
           if (pos < NQ) {
-            if (l0 < NL) ad[l0 * LS + pos] = c0;
-            if (l0 + 1 < NL) ad[(l0 + 1) * LS + pos] = c1;
+            if (l0 < NL) ad[l0 * LSA + pos] = c0;
+            if (l0 + 1 < NL) ad[(l0 + 1) * LSA + pos] = c1;
           }
         }
       }
@@ -289,8 +305,8 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
         const int pt = tid + m * LN_THREADS;
         if (pt < NPT) {
           const int i = pt % NQ, j = (pt / NQ) % NQ, k = pt / (NQ * NQ);
-          const double v = ac[(k * NQ + j) * LS + i] + ac[TS + (k * NQ + i) * LS + j] +
-                           ac[2 * TS + (j * NQ + i) * LS + k];
+          const double v = ac[(k * NQ + j) * LSA + i] + ac[TSA + (k * NQ + i) * LSA + j] +
+                           ac[2 * TSA + (j * NQ + i) * LSA + k];
           re[b * NPT + pt] = (T)(rh[m] + jv[m] * v);
         }
       }
@@ -304,8 +320,17 @@ __global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
 template <typename T, int NQ>
 int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, const T *D,
                  const T *g, const T *jinv, cudaStream_t s) {
-  const size_t smem = lines_smem<NQ>();
-  auto kern = volume_lines_kernel<T, NQ>;
+  // tile strides: 0 = one odd stride (default), 1 = per-kind conflict-free
+  // strides — fewer bank conflicts (397M vs 517M replays at Nq=12) but more
+  // shared memory (Nq=10: one CTA/SM instead of two; Nq=13 does not fit)
+  // and 8-25 % slower (profiles/r01_lines_banks.txt): the kernel is latency-
+  // bound, not bank-bound
+  static const int mode_env = [] {
+    const char *v = getenv("LFB_LINES_STRIDE");
+    return v ? atoi(v) : 0;
+  }();
+  const size_t smem = mode_env ? lines_smem<NQ, 1>() : lines_smem<NQ, 0>();
+  auto kern = mode_env ? volume_lines_kernel<T, NQ, 1> : volume_lines_kernel<T, NQ, 0>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
