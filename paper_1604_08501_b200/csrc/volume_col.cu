@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
   }
 }
 
+#define LFB_ARGS(KS_, EPB_, MB_) KS_, EPB_, MB_
+
 template <typename T, int NQ, int KS, int EPB, int MINB>
 int launch_col(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D, const T *g,
                const T *jinv, cudaStream_t stream) {
@@ -302,33 +304,56 @@ int launch_col(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D, co
 }
 
 // (KS, EPB, MINB) per (dtype, Nq): threads per element = KS Nq^2, EPB
-// elements per CTA, ~128-256 threads per CTA; fp64 halves the points per
-// thread (registers).
+// elements per CTA. Alternative 0 is the default; LFB_COL_ALT=1|2 selects
+// the A/B alternatives (profiles/r01_col_configs.txt).
 template <typename T>
 int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
                  const T *g, const T *jinv, cudaStream_t s) {
+  static const int alt = [] {
+    const char *v = getenv("LFB_COL_ALT");
+    return v ? atoi(v) : 0;
+  }();
   constexpr bool F64 = sizeof(T) == 8;
-#define LFB_COL(NQ_, KS32, EPB32, MB32, KS64, EPB64, MB64)                                   \
-  case NQ_:                                                                                 \
-    if constexpr (F64)                                                                      \
-      return launch_col<T, NQ_, KS64, EPB64, MB64>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);  \
-    else                                                                                    \
-      return launch_col<T, NQ_, KS32, EPB32, MB32>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-  switch (nq) {
-    LFB_COL(2, 1, 32, 4, 1, 32, 2)
-    LFB_COL(3, 1, 14, 4, 1, 14, 2)
-    LFB_COL(4, 1, 8, 4, 2, 4, 2)
-    LFB_COL(5, 1, 5, 4, 1, 5, 2)
-    LFB_COL(6, 2, 2, 4, 2, 2, 2)
-    LFB_COL(7, 1, 3, 4, 2, 1, 2)
-    LFB_COL(8, 2, 1, 4, 4, 1, 2)
-    LFB_COL(9, 3, 1, 2, 3, 1, 2)
-    LFB_COL(10, 2, 1, 2, 5, 1, 1)
-    LFB_COL(11, 3, 1, 2, 4, 1, 1)
-    LFB_COL(12, 3, 1, 1, 4, 1, 1)
-    default: return LFB_ERR_BAD_VARIANT;
+#define LFB_L(NQ_, KS_, EPB_, MB_) \
+  return launch_col<T, NQ_, KS_, EPB_, MB_>(ne, p0, R, gam, q, rhsq, D, g, jinv, s)
+#define LFB_COL3(NQ_, A0, A1, A2)   \
+  case NQ_:                         \
+    if (alt == 1) LFB_L(NQ_, A1);   \
+    if (alt == 2) LFB_L(NQ_, A2);   \
+    LFB_L(NQ_, A0);
+  if constexpr (F64) {
+    switch (nq) {
+      LFB_COL3(2, LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2))
+      LFB_COL3(3, LFB_ARGS(1, 14, 2), LFB_ARGS(1, 14, 2), LFB_ARGS(1, 14, 2))
+      LFB_COL3(4, LFB_ARGS(2, 4, 2), LFB_ARGS(4, 2, 3), LFB_ARGS(1, 8, 2))
+      LFB_COL3(5, LFB_ARGS(5, 1, 4), LFB_ARGS(1, 5, 2), LFB_ARGS(5, 2, 2))
+      LFB_COL3(6, LFB_ARGS(3, 1, 4), LFB_ARGS(2, 2, 2), LFB_ARGS(6, 1, 3))
+      LFB_COL3(7, LFB_ARGS(7, 1, 2), LFB_ARGS(2, 1, 2), LFB_ARGS(4, 1, 3))
+      LFB_COL3(8, LFB_ARGS(4, 1, 2), LFB_ARGS(8, 1, 1), LFB_ARGS(2, 1, 2))
+      LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(9, 1, 1), LFB_ARGS(3, 1, 2))
+      LFB_COL3(10, LFB_ARGS(5, 1, 1), LFB_ARGS(10, 1, 1), LFB_ARGS(5, 1, 1))
+      LFB_COL3(11, LFB_ARGS(4, 1, 1), LFB_ARGS(6, 1, 1), LFB_ARGS(4, 1, 1))
+      LFB_COL3(12, LFB_ARGS(4, 1, 1), LFB_ARGS(6, 1, 1), LFB_ARGS(4, 1, 1))
+      default: return LFB_ERR_BAD_VARIANT;
+    }
+  } else {
+    switch (nq) {
+      LFB_COL3(2, LFB_ARGS(1, 32, 4), LFB_ARGS(1, 32, 4), LFB_ARGS(1, 32, 4))
+      LFB_COL3(3, LFB_ARGS(1, 14, 4), LFB_ARGS(1, 14, 4), LFB_ARGS(1, 14, 4))
+      LFB_COL3(4, LFB_ARGS(4, 2, 6), LFB_ARGS(2, 4, 4), LFB_ARGS(1, 8, 4))
+      LFB_COL3(5, LFB_ARGS(5, 2, 4), LFB_ARGS(5, 1, 8), LFB_ARGS(1, 5, 4))
+      LFB_COL3(6, LFB_ARGS(6, 1, 4), LFB_ARGS(3, 1, 6), LFB_ARGS(2, 2, 4))
+      LFB_COL3(7, LFB_ARGS(2, 1, 4), LFB_ARGS(7, 1, 4), LFB_ARGS(1, 3, 4))
+      LFB_COL3(8, LFB_ARGS(2, 1, 4), LFB_ARGS(4, 1, 4), LFB_ARGS(8, 1, 2))
+      LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(9, 1, 1), LFB_ARGS(3, 2, 1))
+      LFB_COL3(10, LFB_ARGS(2, 1, 2), LFB_ARGS(5, 1, 2), LFB_ARGS(10, 1, 1))
+      LFB_COL3(11, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 2), LFB_ARGS(6, 1, 1))
+      LFB_COL3(12, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(6, 1, 1))
+      default: return LFB_ERR_BAD_VARIANT;
+    }
   }
-#undef LFB_COL
+#undef LFB_COL3
+#undef LFB_L
 }
 
 }  // namespace
