@@ -237,14 +237,15 @@ def e2e_reference_api(nq: int, ne: int, dev, steps: int, warmup: int, seed: int,
 
 
 def emitted_reference_gpu(nq: int, ne: int, dev, steps: int = 20):
-    """The reference's emitted level-8 kernel (tests/golden/emitted/, the
+    """The reference's emitted level-8 kernel (paper_1604_08501_b200/corpus/, the
     text of lf/codegen.py:emit_source) compiled unchanged by NVRTC for
     sm_100a (paper_1604_08501_b200.emitted) and timed on this GPU on the
     same workload at fp32, against the hand-written fp32 kernel."""
     import torch
     from paper_1604_08501_b200 import DeviceFieldState, volume_rhs_device
     from paper_1604_08501_b200.emitted import EmittedKernel
-    path = ROOT / "tests" / "golden" / "emitted" / f"level8_nq{nq}.cl"
+    from paper_1604_08501_b200.emitted import CORPUS
+    path = CORPUS / f"level8_nq{nq}.cl"
     if not path.exists():
         return None
     ds = DeviceFieldState.generate(nq, ne, seed=1, dtype=torch.float32, device=dev)
@@ -272,7 +273,7 @@ def emitted_reference_gpu(nq: int, ne: int, dev, steps: int = 20):
             "ms_per_launch": ms_ref, "ours_f32_ms_per_launch": ms_ours,
             "speedup_ours_f32": ms_ref / ms_ours,
             "kernel": "reference level-8 emitted kernel fused_r_s (lf/codegen.py:443-460 "
-                      "output, tests/golden/emitted/level8_nq8.cl) compiled unchanged by "
+                      "output, paper_1604_08501_b200/corpus/level8_nq8.cl) compiled unchanged by "
                       "NVRTC for sm_100a, launch Ne x (8x8) as emitted"}
 
 

@@ -9,7 +9,7 @@ box; the emitted texts travel instead):
 For every optimisation level 1..8 of the paper's recipe
 (``lf/bench/recipes.py:30-117``, built by ``build_levels``,
 ``lf/bench/driver.py:32-46``) and Nq in NQS, it writes
-``tests/golden/emitted/level<L>_nq<N>.cl`` — the exact text of
+``paper_1604_08501_b200/corpus/level<L>_nq<N>.cl`` — the exact text of
 ``emit_source(kernel, linearize(kernel))`` (``lf/codegen.py:443-460``),
 i.e. what ``loopforge build volume.f90 --emit out.cl`` produces — plus
 ``emitted/index.json`` with, per file, the kernel name, the launch line,
@@ -39,7 +39,7 @@ from loopforge.bench import BenchmarkConfig, make_inputs  # noqa: E402
 from loopforge.codegen import emit_source  # noqa: E402
 from loopforge.schedule import linearize  # noqa: E402
 
-OUT = pathlib.Path(__file__).parent / "emitted"
+OUT = pathlib.Path(__file__).resolve().parents[2] / "paper_1604_08501_b200" / "corpus"
 NQS = (2, 4, 8)
 
 

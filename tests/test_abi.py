@@ -32,6 +32,17 @@ def test_library_exports_every_declared_symbol():
         assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
 
 
+def test_every_header_is_exported_by_its_library():
+    """include/lfb_emitted.h -> liblfb_emitted.so (the emitted-kernel backend)."""
+    from paper_1604_08501_b200 import emitted
+    text = (HEADER.parent / "lfb_emitted.h").read_text()
+    syms = sorted(set(re.findall(r"LFB_API\s+[\w\s\*]*?\b(lfb_\w+)\s*\(", text)))
+    assert syms == sorted(emitted.EXPORTED_SYMBOLS)
+    L = emitted.lib()
+    for name in syms:
+        assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
+
+
 def test_version_and_strings():
     L = _native.lib()
     assert L.lfb_version() >> 16 == 1

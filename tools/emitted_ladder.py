@@ -1,5 +1,5 @@
 """The paper's Table 1 structure on B200: the reference's own emitted kernel
-for every optimisation level (tests/golden/emitted/, compiled unchanged for
+for every optimisation level (paper_1604_08501_b200/corpus/, compiled unchanged for
 sm_100a by paper_1604_08501_b200.emitted) timed next to this package's
 hand-written kernels, on BASELINE config 2 (Nq=8, Ne=32768) in fp32 — the
 precision the emitted kernels are written in (lf/interp.py:71-72).
@@ -26,7 +26,7 @@ sys.path.insert(0, str(ROOT))
 from paper_1604_08501_b200 import DeviceFieldState, volume_rhs_device  # noqa: E402
 from paper_1604_08501_b200.emitted import EmittedKernel  # noqa: E402
 
-EMITTED = ROOT / "tests" / "golden" / "emitted"
+EMITTED = ROOT / "paper_1604_08501_b200" / "corpus"
 
 
 def rel_err(got: torch.Tensor, want: torch.Tensor) -> float:

@@ -37,7 +37,7 @@ ds = DeviceFieldState.generate(8, 64, seed=3)
 # not lfb kernels: run this part unfiltered (`sanitize_run.py emitted`)
 try:
     from paper_1604_08501_b200.emitted import EmittedKernel
-    em = ROOT / "tests" / "golden" / "emitted" / "level8_nq4.cl"
+    em = ROOT / "paper_1604_08501_b200" / "corpus" / "level8_nq4.cl"
     if ONLY_EMITTED:
         ds4 = DeviceFieldState.generate(4, 16, seed=3, dtype=torch.float32)
         EmittedKernel.from_file(em)(ds4)
