@@ -244,3 +244,36 @@ def test_packed_tc_groups_and_tail_against_c_oracle(cuda_device, nq, ne, dtype, 
     want = coracle.volume_f64_eb(nq, q, g, j, d, st.constants)
     err = max_rel_error(coracle.from_element_batched(got), coracle.from_element_batched(want))
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, TOL64), (torch.float32, TOL32)])
+def test_config3_full_size_properties(cuda_device, dtype, tol):
+    """BASELINE config 3/4 size (Nq=8, Ne=262144; 36.5 GB at fp64) on one
+    GPU through size-independent properties: the whole launch equals the
+    4-way element-sharded launches bit for bit (the multi-GPU decomposition),
+    a second launch doubles the increment (linearity), and 128 sampled
+    elements match the C oracle."""
+    from paper_1604_08501_b200.distributed import shard_range
+    nq, ne = 8, 262144
+    ds = DeviceFieldState.generate(nq, ne, seed=5, dtype=dtype)
+    volume_rhs_device(ds)
+    whole = ds.rhsq.clone()
+    ds.rhsq.zero_()
+    for r in range(4):
+        a, b = shard_range(ne, r, 4)
+        volume_rhs_device(ds.shard(a, b))
+    torch.cuda.synchronize()
+    assert torch.equal(whole, ds.rhsq)
+    volume_rhs_device(ds)
+    torch.cuda.synchronize()
+    lin = float(((ds.rhsq - 2 * whole).abs().max() / whole.abs().max()))
+    assert lin <= (1e-14 if dtype == torch.float64 else 1e-6), lin
+    idx = torch.randperm(ne, generator=torch.Generator().manual_seed(0))[:128].sort().values
+    cpu = lambda t: t[idx.to(t.device)].to(torch.float64).cpu().numpy()
+    q, g, j, d = cpu(ds.q), cpu(ds.g), cpu(ds.Jinv), ds.D.to(torch.float64).cpu().numpy()
+    want = coracle.volume_f64_eb(nq, q, g, j, d, ds.constants)
+    got = cpu(whole)
+    err = max_rel_error(coracle.from_element_batched(got), coracle.from_element_batched(want))
+    assert err <= tol, err
+    del ds, whole
+    torch.cuda.empty_cache()
