@@ -202,7 +202,7 @@ template <typename T, int NS, int SUB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
-                     const T *__restrict__ jinv) {
+                     const T *__restrict__ jinv, int pf_extra) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TcSmem<T, NS> &sm = *reinterpret_cast<TcSmem<T, NS> *>(smem_raw);
 
@@ -298,17 +298,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // L2 prefetch (cp.async.bulk.prefetch.L2) of the stage one beyond the
   // shared ring and of the next element's rhsq / Jinv: ~1 element per CTA
   // (~20 MB chip-wide at fp64) in flight ahead of the TMA copies.
+  // pf_extra (LFB_TC_PFD, A/B knob): prefetch distance beyond the default
+  // (q/g one element past the ring, rhsq/Jinv one element ahead)
   auto l2pf = [&](int64_t n) {
-    if (tid == 0 && n + NS < nmine) {
-      const int64_t e = e0 + (n + NS) * G;
+    if (tid == 0 && n + NS + pf_extra < nmine) {
+      const int64_t e = e0 + (n + NS + pf_extra) * G;
       const T *gs;
       uint32_t gb;
       gspan(e, gs, gb);
       prefetch_l2(q + e * SLABQ, SLABQ * sizeof(T));
       prefetch_l2(gs, gb);
     }
-    if (tid == 32 && n + 1 < nmine) {
-      const int64_t e = e0 + (n + 1) * G;
+    if (tid == 32 && n + 1 + pf_extra < nmine) {
+      const int64_t e = e0 + (n + 1 + pf_extra) * G;
       const T *js;
       uint32_t jb;
       jspan(e, js, jb);
@@ -988,6 +990,10 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
   if (sizeof(T) == 8 && qs_env > 0)
     return launch_tc_q<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   const bool lean = lean_env >= 0 ? lean_env != 0 : (PAD_ || (sizeof(T) == 4 && SUB == 8));
+  static const int pfd_env = [] {
+    const char *v = getenv("LFB_TC_PFD");
+    return v ? atoi(v) : 0;
+  }();
   if (lean) return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   const size_t smem = sizeof(TcSmem<T, NS>);
   auto kern = volume_tc_kernel<T, NS, SUB>;
@@ -1000,7 +1006,8 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
     return LFB_ERR_CUDA;
   const int64_t grid = ngroups < sms ? ngroups : sms;
   if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
+  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv,
+                                                     pfd_env);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
