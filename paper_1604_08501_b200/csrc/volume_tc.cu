@@ -726,24 +726,44 @@ int launch_tc_lean(int64_t ngroups, double p0, double R, double gam, const T *q,
 // After phase 1 the dead q stage holds the per-warp S tiles; the next
 // element's q is copied in as soon as phase 2 is done, behind the
 // write-back. Shared memory 104 KB, <= 128 registers.
+// (A/B: both 2-CTA schedules lose to the 1-CTA ring, profiles/r01_ab_qstage.txt,
+// r01_ab_qg.txt; kept as LFB_TC_QSTAGE=1|2 knobs.)
+// GST = true (the "QG" schedule): q AND g through the one stage (68 KB),
+// and after phase 1 the dead stage holds both the S tiles and the 8-field
+// T-out tile, so the next element's copy waits for the write-back (a third
+// barrier per element); 103 KB, two CTAs per SM.
+template <typename T, bool GST>
+struct TcSmemQ;
 template <typename T>
-struct TcSmemQ {
+struct TcSmemQ<T, false> {
   T qstage[8 * TC_NPT];
   double ft[8 * FT_FS];
   double tout[8 * TO_FS];
   unsigned long long bar;
+  __device__ double *touts() { return tout; }
+};
+template <typename T>
+struct TcSmemQ<T, true> {
+  T qstage[17 * TC_NPT];  // q | g
+  double ft[8 * FT_FS];
+  unsigned long long bar;
+  __device__ double *touts() { return reinterpret_cast<double *>(qstage) + TC_WARPS * 2 * ST_SZ; }
 };
 static_assert(TC_WARPS * 2 * ST_SZ * sizeof(double) <= 8 * TC_NPT * sizeof(double),
               "S tiles fit in the dead q stage");
 
-template <typename T, int SUB>
+template <typename T, int SUB, bool GST>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     volume_tc_q_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                        T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                        const T *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TcSmemQ<T> &sm = *reinterpret_cast<TcSmemQ<T> *>(smem_raw);
+  static_assert(!GST || (TC_WARPS * 2 * ST_SZ + 8 * TO_FS) * sizeof(double) <=
+                           17 * TC_NPT * sizeof(T),
+                "S tiles + T-out tile fit in the dead q|g stage");
+  TcSmemQ<T, GST> &sm = *reinterpret_cast<TcSmemQ<T, GST> *>(smem_raw);
   double *const stiles = reinterpret_cast<double *>(sm.qstage);  // [w][2][ST_SZ] after phase 1
+  double *const tout = sm.touts();
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
@@ -801,8 +821,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   __syncthreads();
   auto issue = [&](int64_t n) {
     const int64_t e = e0 + n * G;
-    mbar_expect_tx(bar, SLABQ * sizeof(T));
-    bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
+    if constexpr (GST) {
+      const T *gs;
+      uint32_t gb;
+      span16(g + e * SLABG, SLABG, gs, gb);
+      mbar_expect_tx(bar, SLABQ * sizeof(T) + gb);
+      bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
+      bulk_g2s(sm.qstage + SLABQ, gs, gb, bar);
+    } else {
+      mbar_expect_tx(bar, SLABQ * sizeof(T));
+      bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
+    }
   };
   if (tid == 0 && nmine > 0) issue(0);
 
@@ -830,16 +859,31 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
     {
       double gv[9][2];
+      if constexpr (GST) {
+        mbar_wait(bar, (uint32_t)(n & 1));
+        const T *sg = sm.qstage + SLABQ +
+                      (PAD ? (reinterpret_cast<uintptr_t>(ge) & 15) / sizeof(T) : 0);
 #pragma unroll
-      for (int x = 0; x < 9; ++x) {
-        if (PAD) {
-          gv[x][0] = vld[0] ? (double)__ldg(ge + go + x * NPTR) : 0.0;
-          gv[x][1] = vld[1] ? (double)__ldg(ge + go + x * NPTR + 1) : 0.0;
-        } else {
-          ldg_pair(ge + go + x * NPTR, gv[x][0], gv[x][1]);
+        for (int x = 0; x < 9; ++x) {
+          if (PAD) {
+            gv[x][0] = vld[0] ? (double)sg[go + x * NPTR] : 0.0;
+            gv[x][1] = vld[1] ? (double)sg[go + x * NPTR + 1] : 0.0;
+          } else {
+            ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
+          }
         }
+      } else {
+#pragma unroll
+        for (int x = 0; x < 9; ++x) {
+          if (PAD) {
+            gv[x][0] = vld[0] ? (double)__ldg(ge + go + x * NPTR) : 0.0;
+            gv[x][1] = vld[1] ? (double)__ldg(ge + go + x * NPTR + 1) : 0.0;
+          } else {
+            ldg_pair(ge + go + x * NPTR, gv[x][0], gv[x][1]);
+          }
+        }
+        mbar_wait(bar, (uint32_t)(n & 1));
       }
-      mbar_wait(bar, (uint32_t)(n & 1));
       const T *sq = sm.qstage;
       double qv[8][2];
 #pragma unroll
@@ -916,10 +960,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       }
       acc[b][0] = a0;
       acc[b][1] = a1;
-      sts2(sm.tout + b * TO_FS + toW, q0, q1);
+      sts2(tout + b * TO_FS + toW, q0, q1);
     }
     __syncthreads();  // tout complete; S tiles dead -> the q stage may be refilled
-    if (tid == 0 && n + 1 < nmine) {
+    if (!GST && tid == 0 && n + 1 < nmine) {
       fence_proxy_async();
       issue(n + 1);
     }
@@ -933,7 +977,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
+      const double2 t = *reinterpret_cast<const double2 *>(tout + b * TO_FS + toR);
       if (PAD) {
         if (vld[0]) re[qo + b * NPTR] = (T)((double)re[qo + b * NPTR] + jv[0] * (acc[b][0] + t.x));
         if (vld[1])
@@ -944,14 +988,21 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         st_pair(re + qo + b * NPTR, r0 + jv[0] * (acc[b][0] + t.x), r1 + jv[1] * (acc[b][1] + t.y));
       }
     }
+    if constexpr (GST) {
+      __syncthreads();  // T-out (in the stage) consumed: refill the stage
+      if (tid == 0 && n + 1 < nmine) {
+        fence_proxy_async();
+        issue(n + 1);
+      }
+    }
   }
 }
 
-template <typename T, int SUB>
+template <typename T, int SUB, bool GST>
 int launch_tc_q(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
                 const T *D, const T *g, const T *jinv, cudaStream_t stream) {
-  const size_t smem = sizeof(TcSmemQ<T>);
-  auto kern = volume_tc_q_kernel<T, SUB>;
+  const size_t smem = sizeof(TcSmemQ<T, GST>);
+  auto kern = volume_tc_q_kernel<T, SUB, GST>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
@@ -987,8 +1038,13 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
     const char *v = getenv("LFB_TC_QSTAGE");
     return v ? atoi(v) : 0;
   }();
-  if (sizeof(T) == 8 && qs_env > 0)
-    return launch_tc_q<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+  // (2 = also g through the stage: the QG schedule)
+  if constexpr (sizeof(T) == 8) {
+    if (qs_env == 1)
+      return launch_tc_q<T, SUB, false>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+    if (qs_env == 2)
+      return launch_tc_q<T, SUB, true>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+  }
   const bool lean = lean_env >= 0 ? lean_env != 0 : (PAD_ || (sizeof(T) == 4 && SUB == 8));
   static const int pfd_env = [] {
     const char *v = getenv("LFB_TC_PFD");
