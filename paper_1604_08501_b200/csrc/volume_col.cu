@@ -326,8 +326,8 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
       LFB_COL3(2, LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2))
       LFB_COL3(3, LFB_ARGS(1, 14, 2), LFB_ARGS(1, 14, 2), LFB_ARGS(1, 14, 2))
       LFB_COL3(4, LFB_ARGS(2, 4, 2), LFB_ARGS(4, 2, 3), LFB_ARGS(1, 8, 2))
-      LFB_COL3(5, LFB_ARGS(5, 1, 4), LFB_ARGS(1, 5, 2), LFB_ARGS(5, 2, 2))
-      LFB_COL3(6, LFB_ARGS(3, 1, 4), LFB_ARGS(2, 2, 2), LFB_ARGS(6, 1, 3))
+      LFB_COL3(5, LFB_ARGS(5, 1, 4), LFB_ARGS(5, 1, 5), LFB_ARGS(5, 1, 6))
+      LFB_COL3(6, LFB_ARGS(3, 1, 4), LFB_ARGS(3, 1, 5), LFB_ARGS(6, 1, 4))
       LFB_COL3(7, LFB_ARGS(7, 1, 2), LFB_ARGS(2, 1, 2), LFB_ARGS(4, 1, 3))
       LFB_COL3(8, LFB_ARGS(4, 1, 2), LFB_ARGS(8, 1, 1), LFB_ARGS(2, 1, 2))
       LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(9, 1, 1), LFB_ARGS(3, 1, 2))
@@ -345,8 +345,8 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
       LFB_COL3(6, LFB_ARGS(6, 1, 4), LFB_ARGS(3, 1, 6), LFB_ARGS(2, 2, 4))
       LFB_COL3(7, LFB_ARGS(2, 1, 4), LFB_ARGS(7, 1, 4), LFB_ARGS(1, 3, 4))
       LFB_COL3(8, LFB_ARGS(2, 1, 4), LFB_ARGS(4, 1, 4), LFB_ARGS(8, 1, 2))
-      LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(9, 1, 1), LFB_ARGS(3, 2, 1))
-      LFB_COL3(10, LFB_ARGS(2, 1, 2), LFB_ARGS(5, 1, 2), LFB_ARGS(10, 1, 1))
+      LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(3, 1, 3), LFB_ARGS(9, 1, 1))
+      LFB_COL3(10, LFB_ARGS(2, 1, 2), LFB_ARGS(2, 1, 3), LFB_ARGS(5, 1, 2))
       LFB_COL3(11, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 2), LFB_ARGS(6, 1, 1))
       LFB_COL3(12, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(6, 1, 1))
       default: return LFB_ERR_BAD_VARIANT;
