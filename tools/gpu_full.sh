@@ -14,6 +14,6 @@ timeout 600 python bench.py --ne 262144 --inputs device --steps 40 --warmup 3 --
 timeout 600 python bench.py --ne 262144 --inputs device --dtype f32 --steps 40 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_c4_f32.txt 2>&1
 timeout 900 python bench.py --sweep > gpurun_out/${T}_sweep_f64.txt 2>&1
 timeout 900 python bench.py --sweep --dtype f32 > gpurun_out/${T}_sweep_f32.txt 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_launch.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-emitted > gpurun_out/${T}_ncu_launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_tc -s 3 -c 1 -o gpurun_out/${T}_tc python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_tc32 -s 3 -c 1 -o gpurun_out/${T}_tc32 python bench.py --dtype f32 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_full32.log 2>&1
