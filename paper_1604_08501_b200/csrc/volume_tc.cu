@@ -198,7 +198,11 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
 // A group of P^3 consecutive elements is the same 8*512 / 9*512 value slab
 // as one Nq=8 element, so the TMA and prefetch code is unchanged; only the
 // thread's own-point offsets inside the slab differ. `ne` counts groups.
-template <typename T, int NS, int SUB>
+// MUT != 0 builds a barrier-deletion mutant for the race-detector test
+// (tests/test_mutants.py; cf. the reference's barrier-deletion mutation test,
+// pkg/tests/test_acceptance.py:191-219): 1 drops the F_t barrier, 2 the
+// T-out barrier, 3 the per-warp S-tile __syncwarp.
+template <typename T, int NS, int SUB, int MUT = 0>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         sts2(sm.ft + b * FT_FS + ftW, f0, f1);
       }
     }
-    __syncthreads();  // ft complete; every stage read of this element is done
+    if (MUT != 1) __syncthreads();  // ft complete; every stage read of this element is done
     if (tid == 0 && n + NS < nmine) {
       fence_proxy_async();
       issue(n + NS);
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       double *stl = sm.stile[w][b & 1];
       sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
-      __syncwarp();
+      if (MUT != 3) __syncwarp();
       double fsT[2], ftQ[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       acc[b][1] = a1;
       sts2(sm.tout + b * TO_FS + toW, q0, q1);
     }
-    __syncthreads();  // tout complete
+    if (MUT != 2) __syncthreads();  // tout complete
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const double2 t = *reinterpret_cast<const double2 *>(sm.tout + b * TO_FS + toR);
@@ -1053,6 +1057,15 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
   if (lean) return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   const size_t smem = sizeof(TcSmem<T, NS>);
   auto kern = volume_tc_kernel<T, NS, SUB>;
+  if constexpr (sizeof(T) == 8 && SUB == 8) {  // race-detector test mutants (LFB_TC_MUTANT)
+    static const int mut_env = [] {
+      const char *v = getenv("LFB_TC_MUTANT");
+      return v ? atoi(v) : 0;
+    }();
+    if (mut_env == 1) kern = volume_tc_kernel<T, NS, SUB, 1>;
+    if (mut_env == 2) kern = volume_tc_kernel<T, NS, SUB, 2>;
+    if (mut_env == 3) kern = volume_tc_kernel<T, NS, SUB, 3>;
+  }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
