@@ -82,11 +82,16 @@ class ClockSampler:
                 bit = getattr(p, attr, 0)
                 if bit and (r & bit) and name != "gpu_idle":
                     reasons.add(name)
+        med = statistics.median(s[0] for s in loaded)
+        rejecting = sorted(reasons & REJECTING)
+        # SM clock well below max with no reason at all: a leftover clock lock
+        if self.max_mhz and med < 0.8 * self.max_mhz and not reasons:
+            rejecting.append("clock_stuck_low_no_reason")
         return {
-            "sm_mhz": statistics.median(s[0] for s in loaded),
+            "sm_mhz": med,
             "sm_max_mhz": self.max_mhz,
             "reasons": sorted(reasons),
             "samples": len(loaded),
             "power_w_max": max(s[3] for s in loaded),
-            "rejecting": sorted(reasons & REJECTING),
+            "rejecting": rejecting,
         }
