@@ -61,6 +61,11 @@ constexpr int TC_NPT = 512;
 constexpr int TC_WARPS = 8;
 constexpr int TC_THREADS = 32 * TC_WARPS;
 constexpr int TC_STAGE = 17 * TC_NPT;  // values: q (8 fields) + g (9)
+// packed Nq = 4 groups keep their 8 elements' slabs 64 B apart in the stage
+// (one bulk copy per slab): unpadded, the 4 KB / 2 KB slab stride put the
+// two elements a half-warp touches on the same banks (4-way conflicts)
+template <typename T>
+constexpr int tc_stage_alloc() { return TC_STAGE + 16 * 64 / (int)sizeof(T); }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -160,7 +165,7 @@ constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
 
 template <typename T, int NS>
 struct TcSmem {
-  T stage[NS][TC_STAGE];
+  T stage[NS][tc_stage_alloc<T>()];
   double ft[8 * FT_FS];
   double tout[8 * TO_FS];
   double stile[TC_WARPS][2][ST_SZ];
@@ -234,7 +239,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int ptr = PAD ? (w * SUB + gq) * SUB + 2 * c
                       : ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;     // real point
   const int qo = ur * 8 * NPTR + ptr;  // q / rhsq field 0; fields stride NPTR
-  const int go = ur * 9 * NPTR + ptr;  // g component 0; components stride NPTR
+  // stage layout: SUB = 4 -> per-element slabs padded by EPAD values
+  constexpr int EPAD = (SUB == 4) ? 64 / (int)sizeof(T) : 0;
+  constexpr int SQE = 8 * NPTR + EPAD, SGE = 9 * NPTR + EPAD;
+  constexpr int SGOFF = (SUB == 4) ? 8 * SQE : SLABQ;  // g section of the stage
+  const int sqo = (SUB == 4) ? ur * SQE + ptr : qo;    // own pair in the stage: q
+  const int go = (SUB == 4) ? ur * SGE + ptr : ur * 9 * NPTR + ptr;  // and g
   const int jo = ur * NPTR + ptr;      // Jinv
   bool vld[2];
 #pragma unroll
@@ -293,8 +303,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t gb;
     gspan(e, gs, gb);
     mbar_expect_tx(&bars[s], SLABQ * sizeof(T) + gb);
-    bulk_g2s(sm.stage[s], q + e * SLABQ, SLABQ * sizeof(T), &bars[s]);
-    bulk_g2s(sm.stage[s] + SLABQ, gs, gb, &bars[s]);
+    if constexpr (SUB == 4) {
+#pragma unroll 1
+      for (int u = 0; u < 8; ++u) {
+        bulk_g2s(sm.stage[s] + u * SQE, q + e * SLABQ + u * 8 * NPTR, 8 * NPTR * sizeof(T),
+                 &bars[s]);
+        bulk_g2s(sm.stage[s] + SGOFF + u * SGE, g + e * SLABG + u * 9 * NPTR,
+                 9 * NPTR * sizeof(T), &bars[s]);
+      }
+    } else {
+      bulk_g2s(sm.stage[s], q + e * SLABQ, SLABQ * sizeof(T), &bars[s]);
+      bulk_g2s(sm.stage[s] + SLABQ, gs, gb, &bars[s]);
+    }
   };
   if (tid == 0) {
     for (int64_t n = 0; n < NS && n < nmine; ++n) issue(n);
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t parity = (uint32_t)((n / NS) & 1);
     const int64_t e = e0 + n * G;
     const T *sq = sm.stage[st];
-    const T *sg = sm.stage[st] + SLABQ +
+    const T *sg = sm.stage[st] + SGOFF +
                   (PAD ? (reinterpret_cast<uintptr_t>(g + e * SLABG) & 15) / sizeof(T) : 0);
     T *re = rhsq + e * SLABQ;
 
@@ -361,10 +381,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         if (PAD) {  // padding points: rho = 1, everything else 0 -> zero flux
-          qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
-          qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
+          qv[f][0] = vld[0] ? (double)sq[sqo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
+          qv[f][1] = vld[1] ? (double)sq[sqo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
         } else {
-          ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
+          ld_pair(sq + sqo + f * NPTR, qv[f][0], qv[f][1]);
         }
       }
 #pragma unroll

@@ -138,9 +138,13 @@ constexpr int FT_PS = 72, FT_FS = 8 * FT_PS;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
 constexpr int ST_RS = 8, ST_SZ = 8 * ST_RS;
 
+// packed Nq = 4 groups: per-element slabs 64 B apart in the stage (bank
+// conflicts of the 2 KB slab stride otherwise; see volume_tc.cu)
+constexpr int STAGE_ALLOC = STAGE + 16 * 16;
+
 template <int NS>
 struct Smem32 {
-  float stage[NS][STAGE];
+  float stage[NS][STAGE_ALLOC];
   float ft[8 * FT_FS];
   float tout[8 * TO_FS];
   float stile[WARPS][2][ST_SZ];
@@ -177,7 +181,11 @@ __global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
   const int ptr = PAD ? (w * SUB + gq) * SUB + 2 * c
                       : ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;
   const int qo = ur * 8 * NPTR + ptr;
-  const int go = ur * 9 * NPTR + ptr;
+  constexpr int EPAD = (SUB == 4) ? 16 : 0;  // floats
+  constexpr int SQE = 8 * NPTR + EPAD, SGE = 9 * NPTR + EPAD;
+  constexpr int SGOFF = (SUB == 4) ? 8 * SQE : SLABQ;
+  const int sqo = (SUB == 4) ? ur * SQE + ptr : qo;
+  const int go = (SUB == 4) ? ur * SGE + ptr : ur * 9 * NPTR + ptr;
   const int jo = ur * NPTR + ptr;
   bool vld[2];
 #pragma unroll
@@ -224,8 +232,18 @@ __global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
     uint32_t gb;
     span16(g + e * SLABG, SLABG, gs, gb);
     mbar_expect_tx(&bars[s], SLABQ * sizeof(float) + gb);
-    bulk_g2s(sm.stage[s], q + e * SLABQ, SLABQ * sizeof(float), &bars[s]);
-    bulk_g2s(sm.stage[s] + SLABQ, gs, gb, &bars[s]);
+    if constexpr (SUB == 4) {
+#pragma unroll 1
+      for (int u = 0; u < 8; ++u) {
+        bulk_g2s(sm.stage[s] + u * SQE, q + e * SLABQ + u * 8 * NPTR, 8 * NPTR * sizeof(float),
+                 &bars[s]);
+        bulk_g2s(sm.stage[s] + SGOFF + u * SGE, g + e * SLABG + u * 9 * NPTR,
+                 9 * NPTR * sizeof(float), &bars[s]);
+      }
+    } else {
+      bulk_g2s(sm.stage[s], q + e * SLABQ, SLABQ * sizeof(float), &bars[s]);
+      bulk_g2s(sm.stage[s] + SLABQ, gs, gb, &bars[s]);
+    }
   };
   if (tid == 0) {
     for (int64_t n = 0; n < NS && n < nmine; ++n) issue(n);
@@ -252,7 +270,7 @@ __global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
     const uint32_t parity = (uint32_t)((n / NS) & 1);
     const int64_t e = e0 + n * G;
     const float *sq = sm.stage[st];
-    const float *sg = sm.stage[st] + SLABQ +
+    const float *sg = sm.stage[st] + SGOFF +
                       (PAD ? (reinterpret_cast<uintptr_t>(g + e * SLABG) & 15) / sizeof(float) : 0);
     float *re = rhsq + e * SLABQ;
 
@@ -287,10 +305,10 @@ __global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         if (PAD) {
-          qv[f][0] = vld[0] ? sq[qo + f * NPTR] : (f == 0 ? 1.0f : 0.0f);
-          qv[f][1] = vld[1] ? sq[qo + f * NPTR + 1] : (f == 0 ? 1.0f : 0.0f);
+          qv[f][0] = vld[0] ? sq[sqo + f * NPTR] : (f == 0 ? 1.0f : 0.0f);
+          qv[f][1] = vld[1] ? sq[sqo + f * NPTR + 1] : (f == 0 ? 1.0f : 0.0f);
         } else {
-          const float2 v = *reinterpret_cast<const float2 *>(sq + qo + f * NPTR);
+          const float2 v = *reinterpret_cast<const float2 *>(sq + sqo + f * NPTR);
           qv[f][0] = v.x;
           qv[f][1] = v.y;
         }
