@@ -85,7 +85,7 @@ enum {
                                 contractions on (virtual) Nq=8 planes; f32 storage
                                 computes in fp64 */
     LFB_VARIANT_LINES = 4,   /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
-    LFB_VARIANT_COL = 5      /* Nq 2..12: column owners, FMA in the storage
+    LFB_VARIANT_COL = 5      /* Nq 2..12 (fp32: ..16): column owners, FMA in the storage
                                 precision, fluxes through shared line tiles */
 };
 

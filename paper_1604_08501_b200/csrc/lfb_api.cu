@@ -68,6 +68,7 @@ int resolve(int variant, int bytes, int nq) {
     if (lfb::col_available(bytes, nq)) {
       if (nq == 5 || nq == 6) return LFB_VARIANT_COL;
       if (bytes == 4 && nq >= 9) return LFB_VARIANT_COL;
+      if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }
     if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
     if (lfb::lines_available(bytes, nq)) return LFB_VARIANT_LINES;

@@ -32,6 +32,7 @@
 #include "lfb_math.cuh"
 
 namespace lfb {
+bool col_available(int dtype_bytes, int nq);
 namespace {
 
 __device__ __forceinline__ void col_prefetch_l2(const void *p, uint64_t bytes) {
@@ -349,6 +350,10 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
       LFB_COL3(10, LFB_ARGS(2, 1, 2), LFB_ARGS(2, 1, 3), LFB_ARGS(5, 1, 2))
       LFB_COL3(11, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 2), LFB_ARGS(6, 1, 1))
       LFB_COL3(12, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(6, 1, 1))
+      LFB_COL3(13, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(5, 1, 1))
+      LFB_COL3(14, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(5, 1, 1))
+      LFB_COL3(15, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(3, 1, 1))
+      LFB_COL3(16, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(2, 1, 1))
       default: return LFB_ERR_BAD_VARIANT;
     }
   }
@@ -358,8 +363,13 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
 
 }  // namespace
 
+// fp64 stops at Nq = 12 (register state per column point); fp32 covers 2..16.
+// The file is compiled twice (LFB_COL_DTYPE = 8 | 4, see the Makefile) so the
+// two dtypes' template instances build in parallel.
+#if !defined(LFB_COL_DTYPE) || LFB_COL_DTYPE == 8
 bool col_available(int dtype_bytes, int nq) {
-  return (dtype_bytes == 4 || dtype_bytes == 8) && nq >= 2 && nq <= 12;
+  if (dtype_bytes == 8) return nq >= 2 && nq <= 12;
+  return dtype_bytes == 4 && nq >= 2 && nq <= 16;
 }
 
 int volume_col_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
@@ -368,12 +378,15 @@ int volume_col_f64(int nq, int64_t ne, double p0, double R, double gam, const do
   if (!col_available(8, nq)) return LFB_ERR_BAD_VARIANT;
   return dispatch_col<double>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
+#endif
 
+#if !defined(LFB_COL_DTYPE) || LFB_COL_DTYPE == 4
 int volume_col_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
                    float *rhsq, const float *D, const float *g, const float *jinv,
                    cudaStream_t s) {
   if (!col_available(4, nq)) return LFB_ERR_BAD_VARIANT;
   return dispatch_col<float>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
+#endif
 
 }  // namespace lfb
