@@ -13,14 +13,14 @@ from .diagnostics import (ExecutionError, KernelLaunchError, LoopforgeError,
 from .inputs import (FIELDS, BenchmarkConfig, FieldState, PhysicalConstants,
                      differentiation_matrix, make_inputs)
 from .volume import (DeviceFieldState, interpret_state, max_rel_error,
-                     reference_volume_term, validate_state, volume_rhs_,
-                     volume_rhs_device, volume_term)
+                     reference_volume_term, validate_state, volume_host,
+                     volume_rhs_, volume_rhs_device, volume_term)
 
 __all__ = [
     "FIELDS", "BenchmarkConfig", "FieldState", "PhysicalConstants",
     "differentiation_matrix", "make_inputs", "DeviceFieldState",
     "interpret_state", "max_rel_error", "reference_volume_term",
-    "validate_state", "volume_rhs_", "volume_rhs_device", "volume_term",
+    "validate_state", "volume_host", "volume_rhs_", "volume_rhs_device", "volume_term",
     "LoopforgeError", "ExecutionError", "KernelLaunchError",
     "NativeLibraryMissing",
 ]
