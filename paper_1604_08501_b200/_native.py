@@ -193,6 +193,7 @@ class HostPipeline:
                                     int(compute_bytes), int(device), ctypes.byref(h)),
               "lfb_pipeline_create")
         self._h = h
+        self._run_lock = threading.Lock()  # one pipeline serves one call at a time
         self.nq, self.chunk = int(nq), int(chunk)
         self.host_bytes, self.compute_bytes = int(host_bytes), int(compute_bytes)
 
@@ -205,11 +206,12 @@ class HostPipeline:
     def run(self, mode: int, ne: int, p0: float, R: float, gam: float, q: int, D: int,
             g: int, jinv: int, out: int, stream: int = 0) -> None:
         """Host pointers (ints). Synchronous: the result is in ``out`` on return."""
-        if self._h is None:
-            raise ExecutionError("pipeline is closed")
-        check(lib().lfb_volume_host(self._h, int(mode), int(ne), float(p0), float(R),
-                                    float(gam), q, D, g, jinv, out, stream),
-              "lfb_volume_host")
+        with self._run_lock:
+            if self._h is None:
+                raise ExecutionError("pipeline is closed")
+            check(lib().lfb_volume_host(self._h, int(mode), int(ne), float(p0), float(R),
+                                        float(gam), q, D, g, jinv, out, stream),
+                  "lfb_volume_host")
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and _lib is not None:
