@@ -214,9 +214,16 @@ class HostPipeline:
                   "lfb_volume_host")
 
     def close(self) -> None:
-        if getattr(self, "_h", None) is not None and _lib is not None:
-            _lib.lfb_pipeline_destroy(self._h)
-        self._h = None
+        lock = getattr(self, "_run_lock", None)
+        if lock is not None:
+            lock.acquire()
+        try:
+            if getattr(self, "_h", None) is not None and _lib is not None:
+                _lib.lfb_pipeline_destroy(self._h)
+            self._h = None
+        finally:
+            if lock is not None:
+                lock.release()
 
     def __del__(self):  # pragma: no cover - GC timing
         try:
