@@ -277,3 +277,20 @@ def test_config3_full_size_properties(cuda_device, dtype, tol):
     assert err <= tol, err
     del ds, whole
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nq,ne", [(8, 40), (4, 24), (2, 70), (7, 6), (5, 9), (6, 5), (9, 3),
+                                   (12, 2), (3, 11), (16, 1)])
+def test_arbitrary_differentiation_matrix(cuda_device, nq, ne):
+    """D is an input (lf/codegen.py:361-373), not necessarily the corpus'
+    (n-i)/Nq matrix: a dense random D (not exactly representable in TF32,
+    so the fp32 tensor-core path needs all three split products) through
+    every variant, fp64 <= 1e-12 and fp32 <= 1e-5."""
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=nq + 100))
+    rng = np.random.default_rng(nq)
+    st.D[...] = rng.uniform(-1.0, 1.0, st.D.shape).astype(st.D.dtype)
+    want = O.volume_term_f64_batched(st)
+    for v in _variants(8, nq) + ["auto"]:
+        assert max_rel_error(volume_term(st, dtype=np.float64, variant=v), want) <= TOL64, v
+    for v in _variants(4, nq) + ["auto"]:
+        assert max_rel_error(volume_term(st, dtype=np.float32, variant=v), want) <= TOL32, v
