@@ -1,8 +1,9 @@
-// LFB_VARIANT_TC — Nq = 8: TMA-staged, DMMA-contracted volume kernel.
+// LFB_VARIANT_TC — Nq = 8 (and 2, 4 packed / 5..7 padded into a virtual
+// Nq=8 cube): TMA-staged, DMMA-contracted volume kernel, fp64 storage.
 //
-// Storage type T is double (the fp64 path) or float (the fp32 variant:
-// 136 B/pt of traffic, all arithmetic still fp64 — more accurate than the
-// reference's own f32 pipeline).
+// fp32 storage takes the TF32 split-product kernel of volume_tc32.cu; the
+// float instances below (all arithmetic in fp64) remain as its A/B baseline
+// (LFB_TC32=0).
 //
 // Why this shape (numbers from tools/microbench.cu on
 // B200): the fp64 tensor pipe (DMMA m8n8k4) has the same throughput as the
