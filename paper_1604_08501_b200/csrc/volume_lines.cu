@@ -118,7 +118,7 @@ constexpr int stride_mod16(int nq, int r1, int r2) {
 //     stride = 2 mod 16 -> {4c + g} distinct.
 // (profiles/r01_lines_banks.txt: MODE 0 makes a third of the shared
 // wavefronts bank-conflict replays, but MODE 1 is slower — see launch_lines.)
-template <int NQ, int MODE>
+template <int NQ, int MODE, int TH = LinesCfg<NQ>::THREADS>
 struct LinesGeom {
   static constexpr int NPT = NQ * NQ * NQ;
   static constexpr int NL = NQ * NQ;                 // lines per direction
@@ -127,7 +127,7 @@ struct LinesGeom {
   static constexpr int LT = (NL + 7) / 8;            // line tiles
   static constexpr int LSF = MODE == 0 ? (NQ | 1) : stride_mod16(NQ, 4, 12);
   static constexpr int LSA = MODE == 0 ? (NQ | 1) : stride_mod16(NQ, 2, 2);
-  static constexpr int PPT = (NPT + LinesCfg<NQ>::THREADS - 1) / LinesCfg<NQ>::THREADS;
+  static constexpr int PPT = (NPT + TH - 1) / TH;
   static constexpr int TSF = NL * LSF;               // one flux tile
   static constexpr int TSA = NL * LSA;               // one accumulator tile
 };
@@ -139,13 +139,14 @@ constexpr size_t lines_smem() {
   return sizeof(double) * ((size_t)5 * Gm::NPT + (size_t)3 * (Gm::TSF + Gm::TSA));
 }
 
-template <typename T, int NQ, int MODE>
-__global__ void __launch_bounds__(LinesCfg<NQ>::THREADS, LinesCfg<NQ>::MINB)
+// TH: threads per CTA (LinesCfg default; other values are A/B instances)
+template <typename T, int NQ, int MODE, int TH = LinesCfg<NQ>::THREADS>
+__global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<NQ>::MINB : 1)
     volume_lines_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                         T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                         const T *__restrict__ jinv, int pf_mode, bool hint) {
-  using Gm = LinesGeom<NQ, MODE>;
-  constexpr int LN_THREADS = LinesCfg<NQ>::THREADS;
+  using Gm = LinesGeom<NQ, MODE, TH>;
+  constexpr int LN_THREADS = TH;
   constexpr int NPT = Gm::NPT, NL = Gm::NL, MT = Gm::MT, KS = Gm::KS, LT = Gm::LT;
   constexpr int LSF = Gm::LSF, LSA = Gm::LSA, TSF = Gm::TSF, TSA = Gm::TSA, PPT = Gm::PPT;
   extern __shared__ __align__(16) double lsm[];
@@ -329,8 +330,21 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
     const char *v = getenv("LFB_LINES_STRIDE");
     return v ? atoi(v) : 0;
   }();
+  // LFB_LINES_THREADS (A/B): 384 or 768 threads per CTA instead of the default
+  static const int th_env = [] {
+    const char *v = getenv("LFB_LINES_THREADS");
+    return v ? atoi(v) : 0;
+  }();
   const size_t smem = mode_env ? lines_smem<NQ, 1>() : lines_smem<NQ, 0>();
   auto kern = mode_env ? volume_lines_kernel<T, NQ, 1> : volume_lines_kernel<T, NQ, 0>;
+  int threads = LinesCfg<NQ>::THREADS;
+  if (th_env == 384) {
+    kern = volume_lines_kernel<T, NQ, 0, 384>;
+    threads = 384;
+  } else if (th_env == 768) {
+    kern = volume_lines_kernel<T, NQ, 0, 768>;
+    threads = 768;
+  }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
@@ -339,7 +353,7 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return LFB_ERR_CUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LinesCfg<NQ>::THREADS, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) !=
           cudaSuccess ||
       per_sm < 1)
     return LFB_ERR_LAUNCH;
@@ -360,8 +374,8 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
     const char *v = getenv("LFB_LINES_HINT");
     return v ? atoi(v) : 1;
   }();
-  kern<<<(unsigned)grid, LinesCfg<NQ>::THREADS, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv,
-                                                           pf_env, hint_env != 0);
+  kern<<<(unsigned)grid, threads, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv, pf_env,
+                                             hint_env != 0);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
