@@ -21,7 +21,7 @@ from paper_1604_08501_b200.volume import volume_host  # noqa: E402
 
 ONLY_EMITTED = len(sys.argv) > 1 and sys.argv[1] == "emitted"
 CASES = () if ONLY_EMITTED else ((8, 300), (4, 70), (5, 9), (6, 7), (7, 5), (2, 130), (9, 4),
-                                 (12, 3))
+                                 (12, 3), (3, 5), (13, 2), (16, 1))
 for nq, ne in CASES:
     st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=2))
     for dt in (torch.float64, torch.float32):
