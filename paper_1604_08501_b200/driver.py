@@ -116,6 +116,18 @@ class BenchReport:
             parts.append(f"equiv_rel_err={self.equivalence_error:.3e}")
         return "  ".join(parts)
 
+    def row_csv(self) -> str:
+        err = "" if self.equivalence_error is None else f"{self.equivalence_error:.6e}"
+        pts = self.nq ** 3 * self.ne
+        return (f"{self.level},{self.nq},{self.ne},{self.emitted_ms:.6f},"
+                f"{pts / self.emitted_ms / 1e6:.4f},{self.native_f32_ms:.6f},"
+                f"{self.native_f64_ms:.6f},{err}")
+
+    @staticmethod
+    def csv_header() -> str:
+        return ("level,nq,ne,emitted_ms,emitted_gdofs,native_f32_ms,native_f64_ms,"
+                "equiv_rel_err")
+
 
 def _time(fn, steps: int) -> float:
     fn()
