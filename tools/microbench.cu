@@ -139,6 +139,23 @@ int main() {
     printf("MIX 272 B/pt grid %d x256: %.3f ms, %.1f GB/s, %.2f GDOF/s\n", blocks, ms,
            272.0 * npts / ms / 1e6, npts / ms / 1e6);
   }
+  {  // sustained: the best MIX grid back to back for ~1.5 s, in windows of 200
+    int blocks = sms * 8;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int w = 0; w < 10; ++w) {
+      cudaEventRecord(a);
+      for (int it = 0; it < 200; ++it) mix_kernel<<<blocks, 256>>>(npts, q, g, j, r);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      ms /= 200;
+      printf("MIX sustained window %d: %.3f ms, %.1f GB/s, %.2f GDOF/s\n", w, ms,
+             272.0 * npts / ms / 1e6, npts / ms / 1e6);
+    }
+  }
   {
     long n = npts * 8 / 2;  // double2 count of q
     float ms = time_it([&] { copy_kernel<<<sms * 8, 256>>>(n, (double2 *)q, (double2 *)r); }, 10);
