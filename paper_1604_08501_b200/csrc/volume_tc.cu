@@ -54,6 +54,8 @@ int volume_fused_f32(int, int64_t, float, float, float, const float *, float *, 
 bool fused_available(int dtype_bytes, int nq);
 int volume_tc32_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                     const float *, const float *, cudaStream_t);
+int volume_tc16_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                    const float *, const float *, cudaStream_t);
 
 namespace {
 
@@ -1150,7 +1152,11 @@ int dispatch_tc(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const
 
 }  // namespace
 
+bool tc16_available(int nq);
+
+// fp64: Nq 2, 4..8 (virtual Nq=8 cube); fp32 also 9..16 (volume_tc16.cu)
 bool tc_available(int dtype_bytes, int nq) {
+  if (dtype_bytes == 4 && tc16_available(nq)) return true;
   return (dtype_bytes == 8 || dtype_bytes == 4) && nq >= 2 && nq <= 8 && nq != 3;
 }
 
@@ -1175,6 +1181,8 @@ int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float 
                   float *rhsq, const float *D, const float *g, const float *jinv,
                   cudaStream_t s) {
   if (!tc_available(4, nq)) return LFB_ERR_BAD_VARIANT;
+  if (tc16_available(nq))  // 16x16-plane TF32 kernel: element-aligned access only
+    return volume_tc16_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
   if (!tc_aligned(4, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
   // fp32 storage: TF32 split-product kernel (volume_tc32.cu); LFB_TC32=0
   // selects the fp64-DMMA formulation below (A/B knob)
