@@ -64,11 +64,11 @@ int resolve(int variant, int bytes, int nq) {
     // measured on B200 (profiles/r01_sweep_*.jsonl, profiles/r01_col_sweep_*.jsonl):
     // col wins where tc pads most of its virtual Nq=8 cube (Nq 5, 6) and
     // for fp32 above Nq = 8 (FFMA vs the fp64 DMMA line GEMMs); tc keeps
-    // Nq 2, 4, 7, 8 and fp32 Nq 14..16 (the 16x16-plane TF32 kernel); lines
+    // Nq 2, 4, 7, 8 and fp32 Nq 13..16 (the 16x16-plane TF32 kernel); lines
     // keeps fp64 Nq 9..13 (profiles/r01_col_configs.txt, r01_tc16.txt)
     if (lfb::col_available(bytes, nq)) {
       if (nq == 5 || nq == 6) return LFB_VARIANT_COL;
-      if (bytes == 4 && nq >= 9 && nq <= 13) return LFB_VARIANT_COL;
+      if (bytes == 4 && nq >= 9 && nq <= 12) return LFB_VARIANT_COL;
       if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }
     if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
