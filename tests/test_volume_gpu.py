@@ -294,3 +294,17 @@ def test_arbitrary_differentiation_matrix(cuda_device, nq, ne):
         assert max_rel_error(volume_term(st, dtype=np.float64, variant=v), want) <= TOL64, v
     for v in _variants(4, nq) + ["auto"]:
         assert max_rel_error(volume_term(st, dtype=np.float32, variant=v), want) <= TOL32, v
+
+
+@pytest.mark.parametrize("nq,ne", [(9, 600), (12, 450), (14, 320), (16, 300)])
+def test_tc16_fp32_many_elements_against_c_oracle(cuda_device, nq, ne):
+    """The 16x16-plane TF32 kernel (fp32 storage, Nq 9..16) on enough
+    elements that every CTA runs several persistent iterations."""
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=nq + 3))
+    ds = DeviceFieldState.from_field_state(st, dtype=torch.float32)
+    volume_rhs_device(ds, variant="tc")
+    got = ds.rhsq.to(torch.float64).cpu().numpy()
+    q, g, j, d = coracle.to_element_batched(st)
+    want = coracle.volume_f64_eb(nq, q, g, j, d, st.constants)
+    err = max_rel_error(coracle.from_element_batched(got), coracle.from_element_batched(want))
+    assert err <= TOL32, err
