@@ -136,11 +136,21 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
   const T Rp0 = R / p0;
   __syncthreads();
 
-  T Di[NQ], Dj[NQ];
+  // one own point per thread (KP = 1): its D(k, .) row lives in registers —
+  // loop-invariant, but a shared-memory load cannot be hoisted across the
+  // per-field barriers (+8-9 % at Nq 5, 6; with KP = 2 the extra registers
+  // spill and it loses, profiles/r01_col_configs.txt)
+  constexpr bool DKREG = KP == 1;
+  T Di[NQ], Dj[NQ], Dkr[DKREG ? KP : 1][DKREG ? NQ : 1];
 #pragma unroll
   for (int n = 0; n < NQ; ++n) {
     Di[n] = sD[n * NQ + i];
     Dj[n] = sD[n * NQ + j];
+    if constexpr (DKREG) {
+#pragma unroll
+      for (int kk = 0; kk < KP; ++kk)
+        Dkr[kk][n] = sD[n * NQ + (k0 + kk < NQ ? k0 + kk : 0)];
+    }
   }
   // own points' offsets inside an element slab, and tile positions
   const int col = j * NQ + i;
@@ -250,7 +260,10 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
         const int k = k0 + kk;
         if (k >= NQ) break;
         T acc = T(0);
-        {  // D(k, .) row, broadcast within the warp (one k per warp)
+        if constexpr (DKREG) {  // the thread's D(k, .) rows live in registers
+#pragma unroll
+          for (int n = 0; n < NQ; ++n) acc = fma(Dkr[kk][n], ftc[n], acc);
+        } else {  // D(k, .) row, broadcast within the warp (one k per warp)
           T dk[NQ];
 #pragma unroll
           for (int c = 0; c < (NQ + VEC - 1) / VEC; ++c) {
