@@ -82,11 +82,15 @@ enum {
     LFB_VARIANT_BASIC = 1,   /* column-per-thread, fluxes recomputed per field */
     LFB_VARIANT_FUSED = 2,   /* column-per-thread, fluxes once, register-blocked */
     LFB_VARIANT_TC = 3,      /* Nq 2,4..8: TMA-staged, DMMA (fp64 tensor core)
-                                contractions on (virtual) Nq=8 planes; f32 storage
-                                computes in fp64 */
+                                contractions on (virtual) Nq=8 planes; f32 storage:
+                                TF32 split-product MMAs (Nq 9..16: 16x16 planes) */
     LFB_VARIANT_LINES = 4,   /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
-    LFB_VARIANT_COL = 5      /* Nq 2..12 (fp32: ..16): column owners, FMA in the storage
+    LFB_VARIANT_COL = 5,     /* Nq 2..12 (fp32: ..16): column owners, FMA in the storage
                                 precision, fluxes through shared line tiles */
+    LFB_VARIANT_LT = 6       /* fp64 Nq 9..12: line tiles — R on the DMMA pipe from the
+                                point owner's registers, S/T through swizzled shared
+                                tiles, per-field q/g stages by bulk copy, software-
+                                pipelined over (element, field) */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -16,6 +16,9 @@ import threading
 from .diagnostics import ExecutionError, KernelLaunchError, NativeLibraryMissing
 
 LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "liblfb_volume.so"
+#: test-only build of the same sources plus the tc kernel's barrier-deletion
+#: mutants (tests/test_mutants.py); the package never loads it by itself
+MUTANT_LIB_PATH = LIB_PATH.with_name("liblfb_volume_mutants.so")
 
 LFB_OK = 0
 LFB_ERR_BAD_NQ = 1
@@ -34,8 +37,9 @@ VARIANT_FUSED = 2
 VARIANT_TC = 3
 VARIANT_LINES = 4
 VARIANT_COL = 5
+VARIANT_LT = 6
 VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
-            "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL}
+            "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL, "lt": VARIANT_LT}
 
 MAX_NQ = 16
 
@@ -97,6 +101,19 @@ def _declare(L) -> None:
                                          _vp, _vp, _vp, _vp, _vp]
 
 
+_lib_path = LIB_PATH
+
+
+def use_library(path) -> None:
+    """Bind a different build of the C-ABI library (the mutant test library)
+    instead of LIB_PATH; must precede the first call into the library."""
+    global _lib_path
+    with _lock:
+        if _lib is not None:
+            raise ExecutionError("the native library is already loaded")
+        _lib_path = pathlib.Path(path)
+
+
 def lib():
     """The loaded library (raises NativeLibraryMissing if absent)."""
     global _lib
@@ -104,11 +121,11 @@ def lib():
         return _lib
     with _lock:
         if _lib is None:
-            if not LIB_PATH.exists():
+            if not _lib_path.exists():
                 raise NativeLibraryMissing(
-                    f"{LIB_PATH} is not built; run __graft_entry__.build()")
+                    f"{_lib_path} is not built; run __graft_entry__.build()")
             try:
-                L = ctypes.CDLL(str(LIB_PATH))
+                L = ctypes.CDLL(str(_lib_path))
             except OSError as exc:  # pragma: no cover - environment specific
                 raise NativeLibraryMissing(str(exc)) from exc
             _declare(L)

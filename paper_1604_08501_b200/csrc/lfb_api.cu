@@ -29,6 +29,9 @@ int volume_lines_f64(int, int64_t, double, double, double, const double *, doubl
 int volume_lines_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                      const float *, const float *, cudaStream_t);
 bool lines_available(int dtype_bytes, int nq);
+int volume_lt_f64(int, int64_t, double, double, double, const double *, double *,
+                  const double *, const double *, const double *, cudaStream_t);
+bool lt_available(int dtype_bytes, int nq);
 int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
                    const double *, const double *, const double *, cudaStream_t);
 int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
@@ -72,6 +75,7 @@ int resolve(int variant, int bytes, int nq) {
       if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }
     if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
+    if (bytes == 8 && nq == 12 && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::lines_available(bytes, nq)) return LFB_VARIANT_LINES;
     return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED : LFB_VARIANT_BASIC;
   }
@@ -106,6 +110,9 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
     case LFB_VARIANT_LINES:
       if (!lfb::lines_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lines_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LT:
+      if (!lfb::lt_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lt_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_COL:
       if (!lfb::col_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -136,6 +143,8 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
     case LFB_VARIANT_LINES:
       if (!lfb::lines_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lines_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LT:
+      return LFB_ERR_BAD_VARIANT;
     case LFB_VARIANT_COL:
       if (!lfb::col_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -173,6 +182,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return lfb::lines_available(dtype_bytes, Nq) ? 1 : 0;
     case LFB_VARIANT_COL:
       return lfb::col_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_LT:
+      return lfb::lt_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -190,6 +201,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_TC: return "tc";
     case LFB_VARIANT_LINES: return "lines";
     case LFB_VARIANT_COL: return "col";
+    case LFB_VARIANT_LT: return "lt";
     default: return "unknown";
   }
 }

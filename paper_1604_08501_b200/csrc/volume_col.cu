@@ -291,12 +291,7 @@ template <typename T, int NQ, int KS, int EPB, int MINB>
 int launch_col(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D, const T *g,
                const T *jinv, cudaStream_t stream) {
   using C = ColCfg<T, NQ, KS, EPB>;
-  static const int pf_env = [] {
-    const char *v = getenv("LFB_COL_PREFETCH");
-    return v ? atoi(v) : 1;
-  }();
-  auto kern = pf_env ? volume_col_kernel<T, NQ, KS, EPB, true, MINB>
-                     : volume_col_kernel<T, NQ, KS, EPB, false, MINB>;
+  auto kern = volume_col_kernel<T, NQ, KS, EPB, true, MINB>;
   const size_t smem = C::smem();
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
@@ -318,22 +313,16 @@ int launch_col(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D, co
 }
 
 // (KS, EPB, MINB) per (dtype, Nq): threads per element = KS Nq^2, EPB
-// elements per CTA. Alternative 0 is the default; LFB_COL_ALT=1|2 selects
-// the A/B alternatives (profiles/r01_col_configs.txt).
+// elements per CTA — the measured best of the alternatives in
+// profiles/r01_col_configs.txt.
 template <typename T>
 int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
                  const T *g, const T *jinv, cudaStream_t s) {
-  static const int alt = [] {
-    const char *v = getenv("LFB_COL_ALT");
-    return v ? atoi(v) : 0;
-  }();
   constexpr bool F64 = sizeof(T) == 8;
 #define LFB_L(NQ_, KS_, EPB_, MB_) \
   return launch_col<T, NQ_, KS_, EPB_, MB_>(ne, p0, R, gam, q, rhsq, D, g, jinv, s)
-#define LFB_COL3(NQ_, A0, A1, A2)   \
-  case NQ_:                         \
-    if (alt == 1) LFB_L(NQ_, A1);   \
-    if (alt == 2) LFB_L(NQ_, A2);   \
+#define LFB_COL3(NQ_, A0, A1, A2) \
+  case NQ_:                       \
     LFB_L(NQ_, A0);
   if constexpr (F64) {
     switch (nq) {

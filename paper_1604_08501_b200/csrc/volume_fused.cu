@@ -231,23 +231,9 @@ int launch_fused(int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const T *D,
   using C = FusedCfg<T, NQ>;
   constexpr int EPB = C::EPB;
   const size_t smem = C::smem();
-  // tuning knobs for experiments; defaults = the measured best
-  // (profiles/: 4 CTAs/SM bound, no L2 prefetch — prefetching a whole CTA
-  // group ahead overflowed L2 and doubled DRAM reads)
-  static const int minb_env = [] {
-    const char *v = getenv("LFB_FUSED_MINB");
-    return v ? atoi(v) : 4;
-  }();
-  static const int pf_env = [] {
-    const char *v = getenv("LFB_FUSED_PREFETCH");
-    return v ? atoi(v) : 0;
-  }();
-  auto kern = volume_fused_kernel<T, NQ, EPB, true, 3>;
-  if (minb_env == 2) kern = pf_env ? volume_fused_kernel<T, NQ, EPB, true, 2>
-                                   : volume_fused_kernel<T, NQ, EPB, false, 2>;
-  else if (minb_env == 4) kern = pf_env ? volume_fused_kernel<T, NQ, EPB, true, 4>
-                                        : volume_fused_kernel<T, NQ, EPB, false, 4>;
-  else if (!pf_env) kern = volume_fused_kernel<T, NQ, EPB, false, 3>;
+  // the measured best: 4 CTAs/SM bound, no L2 prefetch (prefetching a whole
+  // CTA group ahead overflowed L2 and doubled DRAM reads)
+  auto kern = volume_fused_kernel<T, NQ, EPB, false, 4>;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)

@@ -321,30 +321,14 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
 template <typename T, int NQ>
 int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhsq, const T *D,
                  const T *g, const T *jinv, cudaStream_t s) {
-  // tile strides: 0 = one odd stride (default), 1 = per-kind conflict-free
-  // strides — fewer bank conflicts (397M vs 517M replays at Nq=12) but more
-  // shared memory (Nq=10: one CTA/SM instead of two; Nq=13 does not fit)
-  // and 8-25 % slower (profiles/r01_lines_banks.txt): the kernel is latency-
-  // bound, not bank-bound
-  static const int mode_env = [] {
-    const char *v = getenv("LFB_LINES_STRIDE");
-    return v ? atoi(v) : 0;
-  }();
-  // LFB_LINES_THREADS (A/B): 384 or 768 threads per CTA instead of the default
-  static const int th_env = [] {
-    const char *v = getenv("LFB_LINES_THREADS");
-    return v ? atoi(v) : 0;
-  }();
-  const size_t smem = mode_env ? lines_smem<NQ, 1>() : lines_smem<NQ, 0>();
-  auto kern = mode_env ? volume_lines_kernel<T, NQ, 1> : volume_lines_kernel<T, NQ, 0>;
-  int threads = LinesCfg<NQ>::THREADS;
-  if (th_env == 384) {
-    kern = volume_lines_kernel<T, NQ, 0, 384>;
-    threads = 384;
-  } else if (th_env == 768) {
-    kern = volume_lines_kernel<T, NQ, 0, 768>;
-    threads = 768;
-  }
+  // one odd tile stride (MODE 0): the per-kind conflict-free strides (MODE 1)
+  // replay fewer bank conflicts (397M vs 517M at Nq=12) but need more shared
+  // memory (Nq=10: one CTA/SM instead of two; Nq=13 does not fit) and were
+  // 8-25 % slower; 384/768 threads per CTA also lost
+  // (profiles/r01_lines_banks.txt)
+  const size_t smem = lines_smem<NQ, 0>();
+  auto kern = volume_lines_kernel<T, NQ, 0>;
+  const int threads = LinesCfg<NQ>::THREADS;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
@@ -360,22 +344,11 @@ int launch_lines(int64_t ne, double p0, double R, double gam, const T *q, T *rhs
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;
-  // L2 prefetch of the next element: 0 none, 1 q + g, 2 q + g + rhsq + Jinv.
-  // Default 0: a whole next element per CTA (360 KB at Nq=12 fp64, 53 MB
-  // chip-wide) thrashes L2 against the per-field re-reads (+42 % DRAM
-  // reads, -15 % speed); without it DRAM traffic is exactly algorithmic
-  // (profiles/r01_lines_l2.txt)
-  static const int pf_env = [] {
-    const char *v = getenv("LFB_LINES_PF");
-    return v ? atoi(v) : 0;
-  }();
-  // L2 eviction hints on the q / g / rhsq loads (1) or plain loads (0)
-  static const int hint_env = [] {
-    const char *v = getenv("LFB_LINES_HINT");
-    return v ? atoi(v) : 1;
-  }();
-  kern<<<(unsigned)grid, threads, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv, pf_env,
-                                             hint_env != 0);
+  // no L2 prefetch of the next element (a whole next element per CTA, 360 KB
+  // at Nq=12 fp64, thrashes L2 against the per-field re-reads: +42 % DRAM
+  // reads, -15 % speed; profiles/r01_lines_l2.txt) and L2 eviction hints on
+  // the q / g / rhsq loads
+  kern<<<(unsigned)grid, threads, smem, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv, 0, true);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }

@@ -1,0 +1,494 @@
+// LFB_VARIANT_LINES, fp64 storage, Nq 9..12 — "line-tile" kernel: the R
+// derivative contracted on the fp64 tensor pipe from the point owner's own
+// registers, S and T exchanged through swizzled shared tiles, ONE CTA
+// barrier per field.
+//
+// Why this shape: at Nq >= 9 one element's q + g (99 KB at
+// Nq=9, 235 KB at Nq=12) no longer fits the tc kernel's staged virtual-cube
+// scheme, and the first `lines` kernel — all three directions as line GEMMs
+// through shared memory, state in shared memory, two barriers per field —
+// was latency-bound at 0.42-0.47 of HBM (profiles/r01_lines_nq12_f64.json:
+// 31 % issue active, 34 % bank-conflict wavefronts).
+//
+// Decomposition (one element per CTA iteration, persistent grid, one CTA of
+// W warps per SM):
+//   * lines (j,k) are cut into tiles of 8; warp w owns R tile w: lane
+//     (g = lane/4, c = lane%4) owns the points (i = c + 4t, line 8w+g),
+//     t < KS = ceil(Nq/4) — stride-4 columns, so every global access of a
+//     warp is 8 lines x 32 contiguous bytes (full sectors);
+//   * R (contract i) is an m8n8k4 GEMM with M = the 8 lines, K = i in the
+//     permuted order (c + 4t), N = output i: the A fragment (row g, k-col c
+//     of step t) is exactly F_r at the lane's own point t, and the output
+//     column permutation (col 2c+s of n-tile u -> i = c + 4(2u+s)) lands
+//     every result on its owner — no data movement at all;
+//   * S (contract j) and T (contract k) cross lines: the owners park F_s and
+//     F_t of one field in two shared tiles X[n][line'] (n = the contracted
+//     index, line' = (k,i) resp. (j,i) with i padded to LP = 4 KS), the
+//     S/T tile owners run C[out][line'] = D(out,n) X[n][line'] as m8n8k4
+//     GEMMs (A = D fragments in registers, B = 4 tile rows x 8 lines), and
+//     write C back to two more tiles that the point owners read;
+//   * tiles are double-buffered across fields, so one __syncthreads per
+//     field separates "flux written" from "GEMM reads it", and the owners
+//     combine field b-1 (rhsq += Jinv (R + S + T)) right after the barrier of
+//     field b (9 barriers per element);
+//   * row stride RS and an XOR swizzle of the 16-byte unit within each
+//     128-byte row segment make the B-fragment reads, the C-fragment pair
+//     writes and the owners' accesses bank-conflict-free for Nq 11, 12
+//     (~13 % extra wavefronts at Nq 9, 10; modelled by tools/lt_banks.py).
+// HBM traffic is the 272 B/pt minimum: q, g, Jinv read once from HBM (the
+// per-field re-reads of q_b and g(b-1, .) hit L2), rhsq read and written
+// once.
+
+#include <stdint.h>
+
+#include "lfb_common.cuh"
+#include "lfb_math.cuh"
+#include "lfb_tma.cuh"
+
+#ifndef LT_RPW
+#define LT_RPW 1
+#endif
+#ifndef LT_PF  // L2 prefetch of the next element's phase-1 inputs: 0 off,
+#define LT_PF 2  // 1 at element start, 2 in region 6 (two fields ahead)
+#endif
+#ifndef LT_HINT  // L2 policies: phase-1 reads evict_last, stage re-reads evict_first
+#define LT_HINT 0
+#endif
+
+namespace lfb {
+namespace {
+
+__device__ __forceinline__ void lt_dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NQ, int RPW>
+struct LtCfg {
+  static constexpr int NPT = NQ * NQ * NQ;
+  static constexpr int KS = (NQ + 3) / 4;            // own points per lane per tile = k-steps
+  static constexpr int NTL = (KS + 1) / 2;           // R output n-tiles
+  static constexpr int MT = (NQ + 7) / 8;            // S/T output m-tiles
+  static constexpr int LP = 4 * KS;                  // S/T line' stride (i padded)
+  static constexpr int LPJ = (NQ % 2) ? NQ + 1 : NQ; // R line stride in j (dummy j = NQ)
+  static constexpr int NLR = NQ * LPJ;               // R lines incl. dummies
+  static constexpr int RT = (NLR + 7) / 8;           // R tiles
+  static constexpr int NT = (NQ * LP + 7) / 8;       // S/T line' tiles
+  // RPW R tiles per warp (1: more warps; 2: more registers per thread)
+  static constexpr int W = (RT + RPW - 1) / RPW;     // warps per CTA
+  static constexpr int JOBS = 2 * NT;                // S and T line' tiles
+  static constexpr int JPW = (JOBS + W - 1) / W;     // GEMM jobs per warp
+  static constexpr int THREADS = 32 * W;
+  static constexpr int ROWS = 4 * KS;                // tile rows (rows >= NQ stay zero)
+  // row stride (doubles) and swizzle, from the bank model (tools/lt_banks.py)
+  // (a multiple of 16 doubles: the swizzle permutes units within 128-byte
+  // segments, so a row must consist of whole segments)
+  static constexpr int RS = (NT * 8 + 15) / 16 * 16;
+  static constexpr int TILE = ROWS * RS;
+  static_assert(RS >= NT * 8, "row holds every line' tile");
+  // field stage slab: a 16-byte aligned superset of one Nq^3 slab
+  static constexpr int GSLAB = (NPT + 3) & ~1;
+  // 2 bufs x {fS, fT, cS, cT} tiles + 2 field stages x {q_b, g(b-1, 0..2)}
+  // slabs + 2 mbarriers
+  // + the per-lane D fragment tables (R: NTL x KS, S/T: MT x KS values per lane)
+  static constexpr int DTAB = (NTL + MT) * KS * 32;
+  static constexpr size_t SMEM =
+      sizeof(double) * (8 * (size_t)TILE + 8 * (size_t)GSLAB + DTAB + 2);
+};
+
+// position of X[n][x] in a tile: the 16-byte unit of x is XOR-swizzled within
+// its 128-byte row segment by a function of the row
+template <int NQ>
+__device__ __forceinline__ int lt_pos(int n, int x) {
+  using C = LtCfg<NQ, 1>;
+  const int h = 4 * (n & 1) + 2 * ((n >> 1) & 1);
+  const int u = x >> 1;
+  const int pu = (u & ~7) | ((u ^ h) & 7);
+  return n * C::RS + 2 * pu + (x & 1);
+}
+
+template <int NQ, int RPW>
+__global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, 1)
+    volume_lt_kernel(int64_t ne, double p0, double R, double gam, const double *__restrict__ q,
+                     double *__restrict__ rhsq, const double *__restrict__ D,
+                     const double *__restrict__ g, const double *__restrict__ jinv) {
+  using C = LtCfg<NQ, RPW>;
+  constexpr int NPT = C::NPT, KS = C::KS, NTL = C::NTL, MT = C::MT, LP = C::LP;
+  constexpr int TILE = C::TILE, NT = C::NT, JPW = C::JPW, W = C::W, GSLAB = C::GSLAB;
+  extern __shared__ __align__(16) double lt_sm[];
+  // tile (buffer b&1, kind): 0 F_s, 1 F_t, 2 C_s, 3 C_t
+  auto tile = [&](int buf, int kind) { return lt_sm + (buf * 4 + kind) * TILE; };
+  // field stage (buffer b&1): slab 0 = q_b, slabs 1..3 = g(b-1, d) of a
+  // momentum field b = 1..3, all bulk-copied two fields ahead
+  double *fst = lt_sm + 8 * TILE;
+  // D fragments, one value per lane: brt[(u*KS + t)*32 + lane], adt[(mt*KS + t)*32 + lane]
+  double *brt = fst + 2 * 4 * GSLAB, *adt = brt + NTL * KS * 32;
+  uint64_t *fbar = reinterpret_cast<uint64_t *>(brt + C::DTAB);
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, c = lane & 3;
+  const double Rp0 = R / p0;
+  // the bulk copies take whole 16-byte units; the last unit of an array may
+  // be half outside it, so values at or beyond its tail are read from global
+  auto tail_of = [](const double *end) {
+    return reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(end) & ~(uintptr_t)15);
+  };
+  const double *gtail = tail_of(g + ne * 9 * NPT), *qtail = tail_of(q + ne * 8 * NPT);
+
+  for (int x = tid; x < 8 * TILE; x += C::THREADS) lt_sm[x] = 0.0;
+  if (tid == 0) {
+    mbar_init(&fbar[0], 1);
+    mbar_init(&fbar[1], 1);
+    mbar_init_fence();
+  }
+
+  // ---- point ownership: R tile r = RPW w + m, line L = 8 r + g = (j, k),
+  //      points i = c + 4t ---------------------------------------------------
+  bool vt[RPW][KS];
+  int pofs[RPW];
+#pragma unroll
+  for (int m = 0; m < RPW; ++m) {
+    const int L = 8 * (RPW * w + m) + gq;
+    const int jj = L % C::LPJ, kk = L / C::LPJ;
+    const bool own = L < C::NLR && jj < NQ;
+    pofs[m] = own ? kk * NQ * NQ + jj * NQ : 0;
+#pragma unroll
+    for (int t = 0; t < KS; ++t) vt[m][t] = own && c + 4 * t < NQ;
+  }
+  // smem positions of own point (m, t) in the S and T layouts
+  auto posS = [&](int m, int t) {
+    const int L = 8 * (RPW * w + m) + gq, jj = L % C::LPJ, kk = L / C::LPJ;
+    return lt_pos<NQ>(jj, kk * LP + c + 4 * t);
+  };
+  auto posT = [&](int m, int t) {
+    const int L = 8 * (RPW * w + m) + gq, jj = L % C::LPJ, kk = L / C::LPJ;
+    return lt_pos<NQ>(kk, jj * LP + c + 4 * t);
+  };
+  // ---- D fragments (D[n*NQ + i] = D(i, n)) --------------------------------
+  //   R: B[k-row c][n-col g] at step t = D(out = slot(u, g), n = c + 4t),
+  //      slot(u, x) = c' + 4(2u + s') for x = 2c' + s';
+  //   S/T: A[g][c] at step t, m-tile mt = D(out = 8 mt + g, n = 4t + c)
+  //   (kept in shared memory: one LDS per use instead of 2 (NTL + MT) KS
+  //   registers held through the kernel)
+  if (w == 0) {
+#pragma unroll
+    for (int u = 0; u < NTL; ++u)
+#pragma unroll
+      for (int t = 0; t < KS; ++t) {
+        const int out = (gq >> 1) + 4 * (2 * u + (gq & 1)), n = c + 4 * t;
+        brt[(u * KS + t) * 32 + lane] = (out < NQ && n < NQ) ? __ldg(D + n * NQ + out) : 0.0;
+      }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int t = 0; t < KS; ++t) {
+        const int out = 8 * mt + gq, n = 4 * t + c;
+        adt[(mt * KS + t) * 32 + lane] = (out < NQ && n < NQ) ? __ldg(D + n * NQ + out) : 0.0;
+      }
+  }
+  __syncthreads();
+
+  // field b of element e into stage buffer b & 1 (thread 0): q_b and, for a
+  // momentum field, g(b-1, d), d = 0..2 — each the 16-byte aligned superset
+  // of its slab, clipped at the array's tail
+  auto issue_field = [&](int64_t e, int b) {
+    uint64_t *bar = &fbar[b & 1];
+    const bool mom = b >= 1 && b <= 3;
+    const double *src[4];
+    uint32_t bytes[4], total = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      if (x > 0 && !mom) break;
+      const double *a0 = x == 0 ? q + (e * 8 + b) * NPT : g + (e * 9 + 3 * (x - 1) + b - 1) * NPT;
+      const double *tl = x == 0 ? qtail : gtail;
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15;
+      uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + NPT) + 15) & ~(uintptr_t)15;
+      if (hi > reinterpret_cast<uintptr_t>(tl)) hi = reinterpret_cast<uintptr_t>(tl);
+      src[x] = reinterpret_cast<const double *>(lo);
+      bytes[x] = (uint32_t)(hi - lo);
+      total += bytes[x];
+    }
+    mbar_expect_tx(bar, total);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      if (x > 0 && !mom) break;
+      if (LT_HINT)
+        bulk_g2s_hint(fst + ((b & 1) * 4 + x) * GSLAB, src[x], bytes[x], bar,
+                      l2_evict_first_policy());
+      else
+        bulk_g2s(fst + ((b & 1) * 4 + x) * GSLAB, src[x], bytes[x], bar);
+    }
+  };
+  // value o of a slab starting at global a0, from its stage copy st. Only
+  // the last element of an odd-Nq array can reach the clipped tail unit, so
+  // every other element reads shared memory unconditionally (a predicated
+  // global fallback in the hot path would hold a long scoreboard on the
+  // destination register even when no lane takes it).
+  auto staged = [](const double *a0, const double *st, const double *tl, int o, bool last) {
+    const int sh = (NPT & 1) ? (int)((reinterpret_cast<uintptr_t>(a0) & 15) >> 3) : 0;
+    if ((NPT & 1) && last) return a0 + o < tl ? st[sh + o] : __ldg(a0 + o);
+    return st[sh + o];
+  };
+
+  // ---- software pipeline over the stream of (element, field) pairs -------
+  // Region f of element e (one CTA barrier at its end) does three
+  // independent things, so one warp's instruction stream interleaves them:
+  //   A  fluxes of field f -> F tiles [f&1], R contraction (registers);
+  //   B  S/T line GEMMs of field f-1 (of the previous element for f = 0):
+  //      F tiles [(f-1)&1] -> C tiles [(f-1)&1];
+  //   C  combine of field f-2 (the previous element's fields 6, 7 for
+  //      f = 0, 1): rhsq += Jinv (R + S + T) from C tiles [(f-2)&1].
+  // Phase 1 of element e (its point-wise state) opens region 0 of e.
+  // Buffer hazards are one barrier apart: F[f&1] is written in region f and
+  // read in f+1, last read (field f-2) in f-1; C[(f-1)&1] is written in f and
+  // read in f+1, last read (field f-3) in f-1. The stage of field f+2 is
+  // issued right after the barrier of region f (its buffer was read in f).
+  auto gemm_st = [&](int buf) {
+#pragma unroll
+    for (int jb = 0; jb < JPW; ++jb) {
+      const int job = w + jb * W;
+      if (job < 2 * NT) {
+        const int kind = job >= NT, lt = kind ? job - NT : job;
+        const double *X = tile(buf, kind);
+        double *Co = tile(buf, 2 + kind);
+        double bv[KS];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) bv[t] = X[lt_pos<NQ>(4 * t + c, 8 * lt + gq)];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < KS; ++t) lt_dmma(c0, c1, adt[(mt * KS + t) * 32 + lane], bv[t]);
+          if (8 * mt + gq < NQ)
+            *reinterpret_cast<double2 *>(Co + lt_pos<NQ>(8 * mt + gq, 8 * lt + 2 * c)) =
+                make_double2(c0, c1);
+        }
+      }
+    }
+  };
+  // rhsq_f += Jinv (R + S + T) at the own points: part = rhsq_f + Jinv R_f
+  auto combine = [&](int buf, double *rf, const double (&part)[RPW][KS],
+                     const double (&jw)[RPW][KS]) {
+    const double *pS = tile(buf, 2), *pT = tile(buf, 3);
+#pragma unroll
+    for (int m = 0; m < RPW; ++m)
+#pragma unroll
+      for (int t = 0; t < KS; ++t)
+        if (vt[m][t])
+          rf[pofs[m] + 4 * t] = fma(jw[m][t], pS[posS(m, t)] + pT[posT(m, t)], part[m][t]);
+  };
+
+  // phase-1 reads of values the field stages read again keep their L2 lines
+  const uint64_t keep = LT_HINT ? l2_evict_last_policy() : 0;
+  auto ld1 = [&](const double *p) { return LT_HINT ? ldg_hint(p, keep) : __ldg(p); };
+
+  int64_t e = blockIdx.x;
+  if (tid == 0 && e < ne) {
+    issue_field(e, 0);
+    issue_field(e, 1);
+  }
+  double part[2][RPW][KS];  // rhsq_f + Jinv R_f of fields f-1, f-2 (by f & 1)
+  double rhn[RPW][KS];      // rhsq of the next field, loaded one region ahead
+  if (e < ne) {
+#pragma unroll
+    for (int m = 0; m < RPW; ++m)
+#pragma unroll
+      for (int t = 0; t < KS; ++t)
+        rhn[m][t] = vt[m][t] ? rhsq[e * 8 * NPT + c + pofs[m] + 4 * t] : 0.0;
+  }
+  double jvp[RPW][KS];      // Jinv of the previous element (its fields 6, 7)
+  double *rep = nullptr;    // rhsq + c of the previous element
+  for (; e < ne; e += gridDim.x) {
+    const double *qe = q + e * 8 * NPT + c;
+    const double *ge = g + e * 9 * NPT + c;
+    double *re = rhsq + e * 8 * NPT + c;
+    const bool lastel = e == ne - 1;
+    const int64_t en = e + gridDim.x;
+    if (LT_PF == 1 && tid == 32 && en < ne) {
+      // next element's phase-1 inputs into L2: rho, U, Theta, g, Jinv
+      prefetch_l2_range(q + en * 8 * NPT, 5ull * NPT * sizeof(double));
+      prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(double));
+      prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(double));
+    }
+
+    // ---- phase 1: W_d = V_d / rho (V_d = sum_a g(a,d) U_a), p, Jinv ----------
+    // every flux is then F_d,b = W_d q_b (+ g(b-1,d) p for b = 1..3); q_0 = rho
+    double Wd[3][RPW][KS], pp[RPW][KS], jv[RPW][KS];
+#pragma unroll
+    for (int m = 0; m < RPW; ++m) {
+      double rho[KS], th[KS], U[3][KS];
+#pragma unroll
+      for (int t = 0; t < KS; ++t) {
+        const int o = pofs[m] + 4 * t;
+        rho[t] = vt[m][t] ? ld1(qe + o) : 1.0;
+        th[t] = vt[m][t] ? __ldg(qe + 4 * NPT + o) : 1.0;
+        jv[m][t] = vt[m][t] ? __ldg(jinv + e * NPT + c + o) : 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) U[a][t] = vt[m][t] ? ld1(qe + (1 + a) * NPT + o) : 0.0;
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double gv[3][KS];
+#pragma unroll
+        for (int t = 0; t < KS; ++t)
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            gv[a][t] = vt[m][t] ? ld1(ge + (3 * d + a) * NPT + pofs[m] + 4 * t) : 0.0;
+#pragma unroll
+        for (int t = 0; t < KS; ++t)
+          Wd[d][m][t] = fma(gv[0][t], U[0][t], fma(gv[1][t], U[1][t], gv[2][t] * U[2][t]));
+      }
+#pragma unroll
+      for (int t = 0; t < KS; ++t) {
+        const double rinv = fast_rcp(rho[t]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) Wd[d][m][t] *= rinv;
+        pp[m][t] = p0 * pos_pow(Rp0 * th[t], gam);
+      }
+    }
+
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      // ---- A: fluxes of field f, R contraction ------------------------------
+      const bool mom = f >= 1 && f <= 3;  // momentum field: pressure term g(f-1, d) p
+      // rhsq of field f arrived during region f-1; issue field f+1's (the next
+      // element's field 0 after f = 7) and pull field f+2's slab into L2
+      double rh[RPW][KS];
+      {
+        double *rnext = f < 7 ? re + (f + 1) * NPT : rhsq + en * 8 * NPT + c;
+        const bool have = f < 7 || en < ne;
+#pragma unroll
+        for (int m = 0; m < RPW; ++m)
+#pragma unroll
+          for (int t = 0; t < KS; ++t) {
+            rh[m][t] = rhn[m][t];
+            rhn[m][t] = (have && vt[m][t]) ? rnext[pofs[m] + 4 * t] : 0.0;
+          }
+        if (tid == 64) {
+          if (f + 2 < 8)
+            prefetch_l2_range(rhsq + (e * 8 + f + 2) * NPT, (uint64_t)NPT * sizeof(double));
+          else if (en < ne)
+            prefetch_l2_range(rhsq + (en * 8 + f - 6) * NPT, (uint64_t)NPT * sizeof(double));
+        }
+      }
+      mbar_wait(&fbar[f & 1], (uint32_t)((f >> 1) & 1));  // 4 fills per buffer per element
+      double pnew[RPW][KS];  // part of field f (slot f & 1 still holds field f-2)
+      {
+        double *fS = tile(f & 1, 0), *fT = tile(f & 1, 1);
+        const double *st = fst + (f & 1) * 4 * GSLAB;
+        const double *qslab = q + (e * 8 + f) * NPT;
+#pragma unroll
+        for (int m = 0; m < RPW; ++m) {
+          double Fr[KS];
+#pragma unroll
+          for (int t = 0; t < KS; ++t) {
+            const int o = pofs[m] + c + 4 * t;  // point index in the slab
+            const double qv = vt[m][t] ? staged(qslab, st, qtail, o, lastel) : 0.0;
+            double fr = Wd[0][m][t] * qv, fs = Wd[1][m][t] * qv, ft = Wd[2][m][t] * qv;
+            if (mom && vt[m][t]) {
+              double gd[3];
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                gd[d] = staged(g + (e * 9 + 3 * d + f - 1) * NPT, st + (1 + d) * GSLAB, gtail,
+                               o, lastel);
+              fr = fma(gd[0], pp[m][t], fr);
+              fs = fma(gd[1], pp[m][t], fs);
+              ft = fma(gd[2], pp[m][t], ft);
+            }
+            Fr[t] = vt[m][t] ? fr : 0.0;
+            if (vt[m][t]) {
+              fS[posS(m, t)] = fs;
+              fT[posT(m, t)] = ft;
+            }
+          }
+          double cr[NTL][2];
+#pragma unroll
+          for (int u = 0; u < NTL; ++u) {
+            cr[u][0] = 0.0;
+            cr[u][1] = 0.0;
+#pragma unroll
+            for (int t = 0; t < KS; ++t)
+              lt_dmma(cr[u][0], cr[u][1], Fr[t], brt[(u * KS + t) * 32 + lane]);
+          }
+#pragma unroll
+          for (int t = 0; t < KS; ++t)
+            pnew[m][t] = fma(jv[m][t], cr[t >> 1][t & 1], rh[m][t]);
+        }
+      }
+      // ---- B: S/T GEMMs of the previous field --------------------------------
+      if (f >= 1 || rep != nullptr) gemm_st((f + 1) & 1);
+      // ---- C: combine the field before that ---------------------------------
+      if (f >= 2) combine(f & 1, re + (f - 2) * NPT, part[f & 1], jv);
+      else if (rep != nullptr) combine(f & 1, rep + (6 + f) * NPT, part[f & 1], jvp);
+#pragma unroll
+      for (int m = 0; m < RPW; ++m)
+#pragma unroll
+        for (int t = 0; t < KS; ++t) part[f & 1][m][t] = pnew[m][t];
+      if (LT_PF == 2 && f == 6 && tid == 32 && en < ne) {
+        prefetch_l2_range(q + en * 8 * NPT, 5ull * NPT * sizeof(double));
+        prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(double));
+        prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(double));
+      }
+      __syncthreads();
+      if (tid == 0) {  // stage of field f+2 (or the next element's fields 0, 1)
+        if (f + 2 < 8) {
+          fence_proxy_async();
+          issue_field(e, f + 2);
+        } else if (en < ne) {
+          fence_proxy_async();
+          issue_field(en, f - 6);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < RPW; ++m)
+#pragma unroll
+      for (int t = 0; t < KS; ++t) jvp[m][t] = jv[m][t];
+    rep = re;
+  }
+  // ---- drain: GEMMs of the last field, combine of the last two ------------
+  if (rep != nullptr) {
+    gemm_st(1);
+    combine(0, rep + 6 * NPT, part[0], jvp);
+    __syncthreads();
+    combine(1, rep + 7 * NPT, part[1], jvp);
+  }
+}
+
+template <int NQ, int RPW>
+int launch_lt(int64_t ne, double p0, double R, double gam, const double *q, double *rhsq,
+              const double *D, const double *g, const double *jinv, cudaStream_t s) {
+  using C = LtCfg<NQ, RPW>;
+  auto kern = volume_lt_kernel<NQ, RPW>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return LFB_ERR_CUDA;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return LFB_ERR_CUDA;
+  const int64_t grid = ne < sms ? ne : sms;
+  if (grid == 0) return LFB_OK;
+  kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  LFB_CHECK_LAUNCH();
+  return LFB_OK;
+}
+
+}  // namespace
+
+bool lt_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq >= 9 && nq <= 12; }
+
+int volume_lt_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                  double *rhsq, const double *D, const double *g, const double *jinv,
+                  cudaStream_t s) {
+  switch (nq) {
+    case 9: return launch_lt<9, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 10: return launch_lt<10, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 11: return launch_lt<11, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 12: return launch_lt<12, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    default: return LFB_ERR_BAD_VARIANT;
+  }
+}
+
+}  // namespace lfb

@@ -1,9 +1,9 @@
 // LFB_VARIANT_TC — Nq = 8 (and 2, 4 packed / 5..7 padded into a virtual
 // Nq=8 cube): TMA-staged, DMMA-contracted volume kernel, fp64 storage.
 //
-// fp32 storage takes the TF32 split-product kernel of volume_tc32.cu; the
-// float instances below (all arithmetic in fp64) remain as its A/B baseline
-// (LFB_TC32=0).
+// fp32 storage takes the TF32 split-product kernel of volume_tc32.cu (the
+// first fp32 variant — this kernel with fp64 arithmetic on f32 storage —
+// reached 34 GDOF/s vs 47; it was removed after that A/B).
 //
 // Why this shape (numbers from tools/microbench.cu on
 // B200): the fp64 tensor pipe (DMMA m8n8k4) has the same throughput as the
@@ -45,12 +45,8 @@ namespace lfb {
 
 int volume_basic_f64(int, int64_t, double, double, double, const double *, double *,
                      const double *, const double *, const double *, cudaStream_t);
-int volume_basic_f32(int, int64_t, float, float, float, const float *, float *, const float *,
-                     const float *, const float *, cudaStream_t);
 int volume_fused_f64(int, int64_t, double, double, double, const double *, double *,
                      const double *, const double *, const double *, cudaStream_t);
-int volume_fused_f32(int, int64_t, float, float, float, const float *, float *, const float *,
-                     const float *, const float *, cudaStream_t);
 bool fused_available(int dtype_bytes, int nq);
 int volume_tc32_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                     const float *, const float *, cudaStream_t);
@@ -58,6 +54,11 @@ int volume_tc16_f32(int, int64_t, float, float, float, const float *, float *, c
                     const float *, const float *, cudaStream_t);
 
 namespace {
+
+#ifdef LFB_EXPERIMENTS
+// test library only: which barrier-deletion mutant launch_tc runs (0 = none)
+int g_tc_mutant = 0;
+#endif
 
 constexpr int TC_NQ = 8;
 constexpr int TC_NPT = 512;
@@ -206,7 +207,8 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
 // A group of P^3 consecutive elements is the same 8*512 / 9*512 value slab
 // as one Nq=8 element, so the TMA and prefetch code is unchanged; only the
 // thread's own-point offsets inside the slab differ. `ne` counts groups.
-// MUT != 0 builds a barrier-deletion mutant for the race-detector test
+// MUT != 0 builds a barrier-deletion mutant for the race-detector test (only
+// in the test library, -DLFB_EXPERIMENTS)
 // (tests/test_mutants.py; cf. the reference's barrier-deletion mutation test,
 // pkg/tests/test_acceptance.py:191-219): 1 drops the F_t barrier, 2 the
 // T-out barrier, 3 the per-warp S-tile __syncwarp.
@@ -214,7 +216,7 @@ template <typename T, int NS, int SUB, int MUT = 0>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
-                     const T *__restrict__ jinv, int pf_extra) {
+                     const T *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TcSmem<T, NS> &sm = *reinterpret_cast<TcSmem<T, NS> *>(smem_raw);
 
@@ -324,20 +326,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   // L2 prefetch (cp.async.bulk.prefetch.L2) of the stage one beyond the
   // shared ring and of the next element's rhsq / Jinv: ~1 element per CTA
-  // (~20 MB chip-wide at fp64) in flight ahead of the TMA copies.
-  // pf_extra (LFB_TC_PFD, A/B knob): prefetch distance beyond the default
-  // (q/g one element past the ring, rhsq/Jinv one element ahead)
+  // (~20 MB chip-wide at fp64) in flight ahead of the TMA copies (a longer
+  // distance measured no better, profiles/r01_ab_tc_prefetch.txt)
   auto l2pf = [&](int64_t n) {
-    if (tid == 0 && n + NS + pf_extra < nmine) {
-      const int64_t e = e0 + (n + NS + pf_extra) * G;
+    if (tid == 0 && n + NS < nmine) {
+      const int64_t e = e0 + (n + NS) * G;
       const T *gs;
       uint32_t gb;
       gspan(e, gs, gb);
       prefetch_l2(q + e * SLABQ, SLABQ * sizeof(T));
       prefetch_l2(gs, gb);
     }
-    if (tid == 32 && n + 1 + pf_extra < nmine) {
-      const int64_t e = e0 + (n + 1 + pf_extra) * G;
+    if (tid == 32 && n + 1 < nmine) {
+      const int64_t e = e0 + (n + 1) * G;
       const T *js;
       uint32_t jb;
       jspan(e, js, jb);
@@ -744,364 +745,43 @@ int launch_tc_lean(int64_t ngroups, double p0, double R, double gam, const T *q,
   return LFB_OK;
 }
 
-// ---------------------------------------------------------------------------
-// QSTAGE schedule (fp64): two CTAs (16 warps) per SM so the kernel stays
-// HBM-bound when the SM clock drops under the power cap (the 1-CTA schedule
-// is 8 % slower at ~1.8 GHz than at 1.965 GHz). Only q goes through a TMA
-// stage (32 KB); g is read straight from global memory into registers (its
-// lines are L2-prefetched one element ahead), rhsq and Jinv at write-back.
-// After phase 1 the dead q stage holds the per-warp S tiles; the next
-// element's q is copied in as soon as phase 2 is done, behind the
-// write-back. Shared memory 104 KB, <= 128 registers.
-// (A/B: both 2-CTA schedules lose to the 1-CTA ring, profiles/r01_ab_qstage.txt,
-// r01_ab_qg.txt; kept as LFB_TC_QSTAGE=1|2 knobs.)
-// GST = true (the "QG" schedule): q AND g through the one stage (68 KB),
-// and after phase 1 the dead stage holds both the S tiles and the 8-field
-// T-out tile, so the next element's copy waits for the write-back (a third
-// barrier per element); 103 KB, two CTAs per SM.
-template <typename T, bool GST>
-struct TcSmemQ;
-template <typename T>
-struct TcSmemQ<T, false> {
-  T qstage[8 * TC_NPT];
-  double ft[8 * FT_FS];
-  double tout[8 * TO_FS];
-  unsigned long long bar;
-  __device__ double *touts() { return tout; }
-};
-template <typename T>
-struct TcSmemQ<T, true> {
-  T qstage[17 * TC_NPT];  // q | g
-  double ft[8 * FT_FS];
-  unsigned long long bar;
-  __device__ double *touts() { return reinterpret_cast<double *>(qstage) + TC_WARPS * 2 * ST_SZ; }
-};
-static_assert(TC_WARPS * 2 * ST_SZ * sizeof(double) <= 8 * TC_NPT * sizeof(double),
-              "S tiles fit in the dead q stage");
-
-template <typename T, int SUB, bool GST>
-__global__ void __launch_bounds__(TC_THREADS, 2)
-    volume_tc_q_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
-                       T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
-                       const T *__restrict__ jinv) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  static_assert(!GST || (TC_WARPS * 2 * ST_SZ + 8 * TO_FS) * sizeof(double) <=
-                           17 * TC_NPT * sizeof(T),
-                "S tiles + T-out tile fit in the dead q|g stage");
-  TcSmemQ<T, GST> &sm = *reinterpret_cast<TcSmemQ<T, GST> *>(smem_raw);
-  double *const stiles = reinterpret_cast<double *>(sm.qstage);  // [w][2][ST_SZ] after phase 1
-  double *const tout = sm.touts();
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, w = tid >> 5;
-  const int gq = lane >> 2, c = lane & 3;
-  const int64_t G = gridDim.x;
-  const int64_t e0 = blockIdx.x;
-  const int64_t nmine = (e0 < ne) ? (ne - 1 - e0) / G + 1 : 0;
-  const double Rp0 = R / p0;
-
-  constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
-  static_assert(SUB >= 2 && SUB <= 8, "virtual Nq=8 cube");
-  constexpr int P = PAD ? 1 : 8 / SUB, NPTR = SUB * SUB * SUB;
-  constexpr int SLABQ = PAD ? 8 * NPTR : 8 * TC_NPT;
-  constexpr int SLABG = PAD ? 9 * NPTR : 9 * TC_NPT;
-  constexpr int SLABJ = PAD ? NPTR : TC_NPT;
-  const int ur = PAD ? 0 : (2 * c) / SUB + P * (gq / SUB) + P * P * (w / SUB);
-  const int ptr = PAD ? (w * SUB + gq) * SUB + 2 * c
-                      : ((w % SUB) * SUB + (gq % SUB)) * SUB + (2 * c) % SUB;
-  const int qo = ur * 8 * NPTR + ptr;
-  const int go = ur * 9 * NPTR + ptr;
-  const int jo = ur * NPTR + ptr;
-  bool vld[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) vld[s] = !PAD || (2 * c + s < SUB && gq < SUB && w < SUB);
-  const int ftW = w * FT_PS + gq * 8 + 2 * c;
-  const int toR = w * TO_PS + gq * 8 + 2 * c;
-  const int toW = gq * TO_PS + w * 8 + 2 * c;
-  int ftR[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) ftR[t] = (c + 4 * t) * FT_PS + w * 8 + gq;
-  auto Dv = [&](int iv, int nv) -> double {
-    if (PAD) return (iv < SUB && nv < SUB) ? (double)__ldg(D + nv * SUB + iv) : 0.0;
-    if (iv / SUB != nv / SUB) return 0.0;
-    return (double)__ldg(D + (nv % SUB) * SUB + (iv % SUB));
-  };
-  double Dr[2], Dst[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    Dr[t] = Dv(gq, 2 * c + t);
-    Dst[t] = Dv(gq, c + 4 * t);
-  }
-  auto span16 = [](const T *p, size_t n, const T *&start, uint32_t &bytes) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uintptr_t lo = a & ~(uintptr_t)15;
-    const uintptr_t hi = (a + n * sizeof(T) + 15) & ~(uintptr_t)15;
-    start = reinterpret_cast<const T *>(lo);
-    bytes = (uint32_t)(hi - lo);
-  };
-
-  uint64_t *bar = reinterpret_cast<uint64_t *>(&sm.bar);
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t n) {
-    const int64_t e = e0 + n * G;
-    if constexpr (GST) {
-      const T *gs;
-      uint32_t gb;
-      span16(g + e * SLABG, SLABG, gs, gb);
-      mbar_expect_tx(bar, SLABQ * sizeof(T) + gb);
-      bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
-      bulk_g2s(sm.qstage + SLABQ, gs, gb, bar);
-    } else {
-      mbar_expect_tx(bar, SLABQ * sizeof(T));
-      bulk_g2s(sm.qstage, q + e * SLABQ, SLABQ * sizeof(T), bar);
-    }
-  };
-  if (tid == 0 && nmine > 0) issue(0);
-
-  for (int64_t n = 0; n < nmine; ++n) {
-    const int64_t e = e0 + n * G;
-    if (n + 1 < nmine) {  // L2 prefetch of the next element
-      const int64_t en = e + G;
-      const T *sp;
-      uint32_t sb_;
-      if (tid == 0) {
-        prefetch_l2(q + en * SLABQ, SLABQ * sizeof(T));
-      } else if (tid == 32) {
-        span16(g + en * SLABG, SLABG, sp, sb_);
-        prefetch_l2(sp, sb_);
-      } else if (tid == 64) {
-        prefetch_l2(rhsq + en * SLABQ, SLABQ * sizeof(T));
-        span16(jinv + en * SLABJ, SLABJ, sp, sb_);
-        prefetch_l2(sp, sb_);
-      }
-    }
-    const T *ge = g + e * SLABG;
-    T *re = rhsq + e * SLABQ;
-
-    // ---- phase 1: g from global (issued before the q wait), q from the stage
-    double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
-    {
-      double gv[9][2];
-      if constexpr (GST) {
-        mbar_wait(bar, (uint32_t)(n & 1));
-        const T *sg = sm.qstage + SLABQ +
-                      (PAD ? (reinterpret_cast<uintptr_t>(ge) & 15) / sizeof(T) : 0);
-#pragma unroll
-        for (int x = 0; x < 9; ++x) {
-          if (PAD) {
-            gv[x][0] = vld[0] ? (double)sg[go + x * NPTR] : 0.0;
-            gv[x][1] = vld[1] ? (double)sg[go + x * NPTR + 1] : 0.0;
-          } else {
-            ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int x = 0; x < 9; ++x) {
-          if (PAD) {
-            gv[x][0] = vld[0] ? (double)__ldg(ge + go + x * NPTR) : 0.0;
-            gv[x][1] = vld[1] ? (double)__ldg(ge + go + x * NPTR + 1) : 0.0;
-          } else {
-            ldg_pair(ge + go + x * NPTR, gv[x][0], gv[x][1]);
-          }
-        }
-        mbar_wait(bar, (uint32_t)(n & 1));
-      }
-      const T *sq = sm.qstage;
-      double qv[8][2];
-#pragma unroll
-      for (int f = 0; f < 8; ++f) {
-        if (PAD) {
-          qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
-          qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
-        } else {
-          ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
-        }
-      }
-      double V2[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        double rinv;
-        point_scalars<T>(qv[0][s], qv[4][s], p0, Rp0, gam, rinv, pP[s]);
-#pragma unroll
-        for (int b = 1; b < 8; ++b) sb[b][s] = qv[b][s] * rinv;
-        V0[s] = gv[0][s] * qv[1][s] + gv[1][s] * qv[2][s] + gv[2][s] * qv[3][s];
-        V1[s] = gv[3][s] * qv[1][s] + gv[4][s] * qv[2][s] + gv[5][s] * qv[3][s];
-        V2[s] = gv[6][s] * qv[1][s] + gv[7][s] * qv[2][s] + gv[8][s] * qv[3][s];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          gr[a][s] = gv[a][s];
-          gs[a][s] = gv[3 + a][s];
-        }
-      }
-      sts2(sm.ft + ftW, V2[0], V2[1]);
-#pragma unroll
-      for (int b = 1; b < 8; ++b) {
-        double f0 = V2[0] * sb[b][0], f1 = V2[1] * sb[b][1];
-        if (b <= 3) {
-          f0 += gv[6 + (b - 1)][0] * pP[0];
-          f1 += gv[6 + (b - 1)][1] * pP[1];
-        }
-        sts2(sm.ft + b * FT_FS + ftW, f0, f1);
-      }
-    }
-    __syncthreads();  // ft complete; the q stage is dead -> S tiles
-    // ---- phase 2 (as in the 1-CTA kernel) -----------------------------------
-    double acc[8][2];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      double fr[2], fs[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (b == 0) {
-          fr[s] = V0[s];
-          fs[s] = V1[s];
-        } else {
-          fr[s] = V0[s] * sb[b][s];
-          fs[s] = V1[s] * sb[b][s];
-          if (b <= 3) {
-            fr[s] += gr[b - 1][s] * pP[s];
-            fs[s] += gs[b - 1][s] * pP[s];
-          }
-        }
-      }
-      double *stl = stiles + (w * 2 + (b & 1)) * ST_SZ;
-      sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
-      __syncwarp();
-      double fsT[2], ftQ[2];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
-        ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
-      }
-      double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        dmma(a0, a1, fr[t], Dr[t]);
-        dmma(a0, a1, Dst[t], fsT[t]);
-        dmma(q0, q1, Dst[t], ftQ[t]);
-      }
-      acc[b][0] = a0;
-      acc[b][1] = a1;
-      sts2(tout + b * TO_FS + toW, q0, q1);
-    }
-    __syncthreads();  // tout complete; S tiles dead -> the q stage may be refilled
-    if (!GST && tid == 0 && n + 1 < nmine) {
-      fence_proxy_async();
-      issue(n + 1);
-    }
-    // ---- write-back (rhsq, Jinv read here: L2-prefetched) -------------------
-    double jv[2];
-    if (PAD) {
-      jv[0] = vld[0] ? (double)__ldg(jinv + e * SLABJ + jo) : 0.0;
-      jv[1] = vld[1] ? (double)__ldg(jinv + e * SLABJ + jo + 1) : 0.0;
-    } else {
-      ldg_pair(jinv + e * SLABJ + jo, jv[0], jv[1]);
-    }
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const double2 t = *reinterpret_cast<const double2 *>(tout + b * TO_FS + toR);
-      if (PAD) {
-        if (vld[0]) re[qo + b * NPTR] = (T)((double)re[qo + b * NPTR] + jv[0] * (acc[b][0] + t.x));
-        if (vld[1])
-          re[qo + b * NPTR + 1] = (T)((double)re[qo + b * NPTR + 1] + jv[1] * (acc[b][1] + t.y));
-      } else {
-        double r0, r1;
-        ld_pair(re + qo + b * NPTR, r0, r1);
-        st_pair(re + qo + b * NPTR, r0 + jv[0] * (acc[b][0] + t.x), r1 + jv[1] * (acc[b][1] + t.y));
-      }
-    }
-    if constexpr (GST) {
-      __syncthreads();  // T-out (in the stage) consumed: refill the stage
-      if (tid == 0 && n + 1 < nmine) {
-        fence_proxy_async();
-        issue(n + 1);
-      }
-    }
-  }
-}
-
-template <typename T, int SUB, bool GST>
-int launch_tc_q(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
-                const T *D, const T *g, const T *jinv, cudaStream_t stream) {
-  const size_t smem = sizeof(TcSmemQ<T, GST>);
-  auto kern = volume_tc_q_kernel<T, SUB, GST>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return LFB_ERR_CUDA;
-  int dev = 0, sms = 0, per_sm = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem) !=
-          cudaSuccess)
-    return LFB_ERR_CUDA;
-  if (per_sm < 1) return LFB_ERR_LAUNCH;
-  const int64_t slots = (int64_t)sms * per_sm;
-  const int64_t grid = ngroups < slots ? ngroups : slots;
-  if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
-  LFB_CHECK_LAUNCH();
-  return LFB_OK;
-}
-
 template <typename T, int NS, int SUB>
 int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
               const T *D, const T *g, const T *jinv, cudaStream_t stream) {
   // Schedule choice from the A/B on this pool (profiles/r01_ab_lean.txt):
-  // the 2-CTA LEAN schedule wins for the zero-padded Nq = 5..7 (+8..10 %)
-  // and marginally for fp32 Nq=8 (+1.6 %); the 1-CTA schedule wins for fp64
-  // Nq=8 (+8 %) and Nq=4. LFB_TC_LEAN=0|1 overrides (A/B knob).
-  static const int lean_env = [] {
-    const char *v = getenv("LFB_TC_LEAN");
-    return v ? atoi(v) : -1;
-  }();
+  // the 2-CTA LEAN schedule wins for the zero-padded Nq = 5..7 (+8..10 %);
+  // the 1-CTA ring wins for Nq = 8 (+8 %) and the packed Nq = 4, 2. (Two
+  // further 2-CTA schedules for Nq=8 — q staged, g from L2; q and g staged,
+  // T-out in the dead stage — lost to the ring, profiles/r01_ab_qstage.txt,
+  // r01_ab_qg.txt, and were removed.)
   constexpr bool PAD_ = !(SUB == 8 || SUB == 4 || SUB == 2);
-  // LFB_TC_QSTAGE=1: the 2-CTA q-staged schedule (fp64 A/B knob)
-  static const int qs_env = [] {
-    const char *v = getenv("LFB_TC_QSTAGE");
-    return v ? atoi(v) : 0;
-  }();
-  // (2 = also g through the stage: the QG schedule)
-  if constexpr (sizeof(T) == 8) {
-    if (qs_env == 1)
-      return launch_tc_q<T, SUB, false>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
-    if (qs_env == 2)
-      return launch_tc_q<T, SUB, true>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+  if constexpr (PAD_) {
+    return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+  } else {
+    const size_t smem = sizeof(TcSmem<T, NS>);
+    auto kern = volume_tc_kernel<T, NS, SUB>;
+#ifdef LFB_EXPERIMENTS
+    // barrier-deletion mutants for the race-detector test (tests/test_mutants.py),
+    // built only into the test library liblfb_volume_mutants.so
+    if constexpr (SUB == 8) {
+      if (g_tc_mutant == 1) kern = volume_tc_kernel<T, NS, SUB, 1>;
+      if (g_tc_mutant == 2) kern = volume_tc_kernel<T, NS, SUB, 2>;
+      if (g_tc_mutant == 3) kern = volume_tc_kernel<T, NS, SUB, 3>;
+    }
+#endif
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return LFB_ERR_CUDA;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return LFB_ERR_CUDA;
+    const int64_t grid = ngroups < sms ? ngroups : sms;
+    if (grid == 0) return LFB_OK;
+    kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
+    LFB_CHECK_LAUNCH();
+    return LFB_OK;
   }
-  const bool lean = lean_env >= 0 ? lean_env != 0 : (PAD_ || (sizeof(T) == 4 && SUB == 8));
-  static const int pfd_env = [] {
-    const char *v = getenv("LFB_TC_PFD");
-    return v ? atoi(v) : 0;
-  }();
-  if (lean) return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
-  const size_t smem = sizeof(TcSmem<T, NS>);
-  auto kern = volume_tc_kernel<T, NS, SUB>;
-  if constexpr (sizeof(T) == 8 && SUB == 8) {  // race-detector test mutants (LFB_TC_MUTANT)
-    static const int mut_env = [] {
-      const char *v = getenv("LFB_TC_MUTANT");
-      return v ? atoi(v) : 0;
-    }();
-    if (mut_env == 1) kern = volume_tc_kernel<T, NS, SUB, 1>;
-    if (mut_env == 2) kern = volume_tc_kernel<T, NS, SUB, 2>;
-    if (mut_env == 3) kern = volume_tc_kernel<T, NS, SUB, 3>;
-  }
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return LFB_ERR_CUDA;
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return LFB_ERR_CUDA;
-  const int64_t grid = ngroups < sms ? ngroups : sms;
-  if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv,
-                                                     pfd_env);
-  LFB_CHECK_LAUNCH();
-  return LFB_OK;
 }
 
 template <typename T>
@@ -1116,13 +796,6 @@ int tail_launch<double>(int nq, int64_t ne, double p0, double R, double gam, con
                                 : volume_basic_f64(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
-template <>
-int tail_launch<float>(int nq, int64_t ne, float p0, float R, float gam, const float *q,
-                       float *rhsq, const float *D, const float *g, const float *jinv,
-                       cudaStream_t s) {
-  return fused_available(4, nq) ? volume_fused_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s)
-                                : volume_basic_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-}
 
 // Full groups of P^3 elements go through the packed tensor-core kernel; the
 // < P^3 leftover elements (Nq = 4: < 8, Nq = 2: < 64) take the fused/basic
@@ -1151,6 +824,12 @@ int dispatch_tc(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, const
 }
 
 }  // namespace
+
+#ifdef LFB_EXPERIMENTS
+extern "C" __attribute__((visibility("default"))) void lfb_test_set_tc_mutant(int m) {
+  g_tc_mutant = m;
+}
+#endif
 
 bool tc16_available(int nq);
 
@@ -1181,17 +860,16 @@ int volume_tc_f32(int nq, int64_t ne, float p0, float R, float gam, const float 
                   float *rhsq, const float *D, const float *g, const float *jinv,
                   cudaStream_t s) {
   if (!tc_available(4, nq)) return LFB_ERR_BAD_VARIANT;
-  if (tc16_available(nq))  // 16x16-plane TF32 kernel: element-aligned access only
+  if (tc16_available(nq)) {  // 16x16-plane TF32 kernel: paired accesses need 8-byte
+    // alignment for even Nq (element alignment is all validate() guarantees)
+    const uintptr_t a = reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(rhsq) |
+                        reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(jinv);
+    if ((nq % 2) == 0 && (a & 7)) return LFB_ERR_MISALIGNED;
     return volume_tc16_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  }
   if (!tc_aligned(4, q, rhsq, g, jinv)) return LFB_ERR_MISALIGNED;
-  // fp32 storage: TF32 split-product kernel (volume_tc32.cu); LFB_TC32=0
-  // selects the fp64-DMMA formulation below (A/B knob)
-  static const int tc32_env = [] {
-    const char *v = getenv("LFB_TC32");
-    return v ? atoi(v) : 1;
-  }();
-  if (tc32_env) return volume_tc32_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
-  return dispatch_tc<float, 3>(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  // fp32 storage: the TF32 split-product kernel (volume_tc32.cu)
+  return volume_tc32_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
 }
 
 }  // namespace lfb

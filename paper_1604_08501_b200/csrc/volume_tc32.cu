@@ -447,10 +447,6 @@ int launch_tc32(int64_t ngroups, float p0, float R, float gam, const float *q, f
 int volume_tc32_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q,
                     float *rhsq, const float *D, const float *g, const float *jinv,
                     cudaStream_t s) {
-  static const int ns_env = [] {
-    const char *v = getenv("LFB_TC32_NS");
-    return v ? atoi(v) : 2;
-  }();
   const bool pad = !(nq == 8 || nq == 4 || nq == 2);
   const int64_t pe = pad ? 1 : (int64_t)(8 / nq) * (8 / nq) * (8 / nq);
   const int64_t groups = pad ? (ne > 0 ? ne - 1 : 0) : ne / pe;
@@ -469,8 +465,9 @@ int volume_tc32_f32(int nq, int64_t ne, float p0, float R, float gam, const floa
         default: return (int)LFB_ERR_BAD_VARIANT;
       }
     };
-    rc = ns_env == 3 ? run(std::integral_constant<int, 3>{})
-                     : run(std::integral_constant<int, 2>{});
+    // 2-stage ring, two CTAs per SM (a 1-CTA 3-stage ring measured slower,
+    // profiles/r01_ab_tc32.txt)
+    rc = run(std::integral_constant<int, 2>{});
   }
   if (rc != LFB_OK || done == ne) return rc;
   return volume_col_f32(nq, ne - done, p0, R, gam, q + done * 8 * npt, rhsq + done * 8 * npt, D,

@@ -5,7 +5,12 @@ path.
 * ``equivalence_error(kernels, cfg)`` — ``lf/bench/driver.py:94-100``: run a
   kernel pipeline on ``cfg``'s inputs (in place, ``rhsq += v``, float32 —
   the interpreter's contract, ``lf/interp.py:71-72``) and return the
-  per-field max-norm relative error against ``reference_volume_term``.
+  per-field max-norm relative error against an INDEPENDENT CPU reference
+  (``want``, as ``lf/bench/driver.py:98`` uses the reference's numpy
+  oracle): by default the unmodified reference's own
+  ``loopforge.bench.reference_volume_term`` (``baseline/_ref``), or any
+  callable passed as ``reference=`` (the tests pass the pinned oracle).
+  Never this package's own GPU path, so common-mode errors cannot pass.
   The reference interprets its kernel IR; here a "kernel" is either one of
   the reference's emitted kernels compiled for sm_100a (``EmittedKernel``)
   or a native variant name (``"auto"``, ``"tc"``, ``"col"``, ...), both run
@@ -22,7 +27,10 @@ path.
 
 from __future__ import annotations
 
+import importlib
 import json
+import pathlib
+import sys
 from dataclasses import dataclass
 
 import torch
@@ -30,8 +38,30 @@ import torch
 from .diagnostics import ExecutionError
 from .emitted import CORPUS, EmittedKernel
 from .inputs import BenchmarkConfig, make_inputs
-from .volume import (DeviceFieldState, max_rel_error, reference_volume_term,
-                     volume_rhs_device)
+from .volume import DeviceFieldState, max_rel_error, volume_rhs_device
+
+#: where ``pip install --target`` puts the unmodified reference
+REFERENCE_INSTALL = pathlib.Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+
+
+def independent_reference():
+    """The unmodified reference's ``reference_volume_term``
+    (``lf/bench/reference.py:36-70``): importable ``loopforge``, else the
+    ``baseline/_ref`` install. Raises ExecutionError when neither exists —
+    there is no silent substitute."""
+    try:
+        return importlib.import_module("loopforge.bench").reference_volume_term
+    except ImportError:
+        pass
+    if (REFERENCE_INSTALL / "loopforge").is_dir():
+        sys.path.append(str(REFERENCE_INSTALL))
+        try:
+            return importlib.import_module("loopforge.bench").reference_volume_term
+        except ImportError:
+            pass
+    raise ExecutionError("equivalence_error needs an independent CPU reference: pass "
+                         "reference=<callable(state) -> increment> or install the "
+                         "reference into baseline/_ref")
 
 
 def corpus_index() -> dict:
@@ -60,20 +90,22 @@ def _run(kernels, ds: DeviceFieldState) -> None:
             raise ExecutionError(f"not a kernel: {k!r}")
 
 
-def equivalence_error(kernels, cfg: BenchmarkConfig, device=None) -> float:
+def equivalence_error(kernels, cfg: BenchmarkConfig, device=None,
+                      reference=None) -> float:
     """Max relative error of the kernel pipeline (on the GPU, f32, in place)
-    against ``reference_volume_term`` on cfg's inputs."""
+    against the independent CPU ``reference(state)`` on cfg's inputs."""
     state = make_inputs(cfg)
-    want = reference_volume_term(state)
+    want = (reference or independent_reference())(state)
     ds = DeviceFieldState.from_field_state(state, dtype=torch.float32, device=device)
     _run(list(kernels), ds)
     got = ds.rhsq_logical()
     return max_rel_error(got - state.rhsq, want)
 
 
-def full_check(levels, nqs, nes, seeds, tolerance: float = 1e-5):
+def full_check(levels, nqs, nes, seeds, tolerance: float = 1e-5, reference=None):
     """Equivalence suite over the grid; yields ``(cfg, err, ok)``; levels the
     reference cannot emit yield ``err = None, ok = False``."""
+    reference = reference or independent_reference()
     for nq in nqs:
         for level in levels:
             try:
@@ -86,7 +118,7 @@ def full_check(levels, nqs, nes, seeds, tolerance: float = 1e-5):
             for ne in nes:
                 for seed in seeds:
                     cfg = BenchmarkConfig(nq=nq, ne=ne, level=level, seed=seed)
-                    err = equivalence_error([k], cfg)
+                    err = equivalence_error([k], cfg, reference=reference)
                     yield cfg, err, err <= tolerance
             k.close()
 
@@ -143,7 +175,7 @@ def _time(fn, steps: int) -> float:
 
 
 def run_benchmark(cfg: BenchmarkConfig, check: bool | None = None,
-                  steps: int = 10) -> BenchReport:
+                  steps: int = 10, reference=None) -> BenchReport:
     """Time cfg.level's emitted kernel and this package's kernels on the GPU
     on device-generated inputs of cfg's shape; optionally verify (always when
     Nq <= 4 unless disabled, like the reference)."""
@@ -157,7 +189,7 @@ def run_benchmark(cfg: BenchmarkConfig, check: bool | None = None,
     del b, ds32, ds64
     if check is None:
         check = cfg.nq <= 4
-    err = equivalence_error([k], cfg) if check else None
+    err = equivalence_error([k], cfg, reference=reference) if check else None
     src = k.source
     k.close()
     return BenchReport(level=cfg.level, nq=cfg.nq, ne=cfg.ne, emitted_ms=emitted_ms,
@@ -165,5 +197,5 @@ def run_benchmark(cfg: BenchmarkConfig, check: bool | None = None,
                        equivalence_error=err, source=src)
 
 
-__all__ = ["corpus_index", "emitted_level", "equivalence_error", "full_check",
+__all__ = ["independent_reference", "corpus_index", "emitted_level", "equivalence_error", "full_check",
            "run_benchmark", "BenchReport"]

@@ -63,11 +63,29 @@ def _device(device) -> torch.device:
     return dev
 
 
+def state_arrays(state) -> dict:
+    """The five arrays of a FieldState — this package's mirror or the
+    reference's own ``loopforge.bench.FieldState`` (``lf/bench/inputs.py:
+    52-74``), which has ``arrays()`` and ``constants`` but none of the
+    mirror's conveniences (``nq``, ``ne``, ``astype``): entry points use only
+    what both define."""
+    if hasattr(state, "arrays"):
+        return state.arrays()
+    return {n: getattr(state, n, None) for n in ("q", "rhsq", "D", "g", "Jinv")}
+
+
+def state_constants(state) -> PhysicalConstants:
+    c = getattr(state, "constants", None)
+    return PhysicalConstants() if c is None else c
+
+
 def validate_state(state: FieldState, nq: int | None = None,
                    ne: int | None = None, dtype=None) -> tuple[int, int]:
     """Shape/dtype checks with the reference's error behaviour
-    (``lf/interp.py:51-74``: ``ExecutionError`` naming the array)."""
-    arrays = state.arrays()
+    (``lf/interp.py:51-74``: ``ExecutionError`` naming the array).
+    Returns ``(Nq, Ne)`` read from the arrays, never from attributes only
+    this package's FieldState mirror has."""
+    arrays = state_arrays(state)
     for name in ("q", "rhsq", "D", "g", "Jinv"):
         if arrays.get(name) is None:
             raise ExecutionError(f"missing array argument {name!r}")
@@ -134,11 +152,11 @@ class DeviceFieldState:
         """Upload the reference's C-order arrays ([i,j,k,b,e], element
         fastest) as they are and convert them on the device (native
         layout kernel, cast fused) to the element-batched layout."""
-        validate_state(state)
+        nq, ne = validate_state(state)
+        arrays = state_arrays(state)
         dev = _device(device)
         dt = _torch_dtype(dtype)
         out_bytes = 8 if dt == torch.float64 else 4
-        nq, ne = state.nq, state.ne
         with torch.cuda.device(dev):
             s = stream or torch.cuda.current_stream(dev)
 
@@ -149,15 +167,16 @@ class DeviceFieldState:
                 _native.reverse_axes_ptr(True, src.element_size(), out_bytes, dims,
                                          a.shape[-1], src.data_ptr(), out.data_ptr(),
                                          s.cuda_stream)
-                src.record_stream(s)  # staging buffer stays valid until the kernel ran
+                if src.is_cuda:  # staging buffer stays valid until the kernel ran
+                    src.record_stream(s)
                 return out
 
-            ds = cls(q=up(state.q, (ne, 8, nq, nq, nq)),
-                     rhsq=up(state.rhsq, (ne, 8, nq, nq, nq)),
-                     D=up(state.D, (nq, nq)),
-                     g=up(state.g, (ne, 3, 3, nq, nq, nq)),
-                     Jinv=up(state.Jinv, (ne, nq, nq, nq)),
-                     constants=state.constants)
+            ds = cls(q=up(arrays["q"], (ne, 8, nq, nq, nq)),
+                     rhsq=up(arrays["rhsq"], (ne, 8, nq, nq, nq)),
+                     D=up(arrays["D"], (nq, nq)),
+                     g=up(arrays["g"], (ne, 3, 3, nq, nq, nq)),
+                     Jinv=up(arrays["Jinv"], (ne, nq, nq, nq)),
+                     constants=state_constants(state))
         return ds
 
     @classmethod
@@ -265,10 +284,10 @@ def volume_term(state: FieldState, c: PhysicalConstants | None = None, *,
                 dtype=np.float64, device=None, variant="auto") -> np.ndarray:
     """The rhsq increment v at ``dtype`` (state.rhsq unchanged), logical
     layout ``[Nq, Nq, Nq, 8, Ne]``."""
-    nq, ne = validate_state(state)
+    validate_state(state)
     ds = DeviceFieldState.from_field_state(state, dtype=dtype, device=device)
     ds.rhsq.zero_()
-    volume_rhs_device(ds, variant=variant, constants=c or state.constants)
+    volume_rhs_device(ds, variant=variant, constants=c or state_constants(state))
     return ds.rhsq_logical()
 
 
@@ -314,7 +333,7 @@ def volume_host(state: FieldState, c: PhysicalConstants | None = None, *,
     Every array must share one dtype (f32 or f64); ``out`` (increment mode)
     may be a preallocated C-order array of that dtype, e.g. page-locked."""
     nq, ne = validate_state(state)
-    arrays = state.arrays()
+    arrays = state_arrays(state)
     hdt = arrays["q"].dtype
     for name in ("q", "rhsq", "D", "g", "Jinv"):
         a = arrays[name]
@@ -326,12 +345,13 @@ def volume_host(state: FieldState, c: PhysicalConstants | None = None, *,
     cb = np.dtype(compute_dtype).itemsize
     if cb not in (4, 8):
         raise ExecutionError(f"unsupported compute dtype {compute_dtype!r}")
-    c = c or state.constants
+    c = c or state_constants(state)
+    q = arrays["q"]
     if accumulate:
-        target = state.rhsq
+        target = arrays["rhsq"]
     else:
-        target = np.empty(state.q.shape, hdt) if out is None else out
-        if target.shape != state.q.shape or target.dtype != hdt or \
+        target = np.empty(q.shape, hdt) if out is None else out
+        if target.shape != q.shape or target.dtype != hdt or \
                 not target.flags.c_contiguous:
             raise ExecutionError("out must be a C-contiguous array shaped like q")
     if ne == 0:
@@ -342,8 +362,8 @@ def volume_host(state: FieldState, c: PhysicalConstants | None = None, *,
     dev = _device(device)
     s = stream or torch.cuda.current_stream(dev)
     p.run(_native.HOST_ACCUMULATE if accumulate else _native.HOST_INCREMENT, ne,
-          c.p0, c.R, c.gamma, state.q.ctypes.data, state.D.ctypes.data,
-          state.g.ctypes.data, state.Jinv.ctypes.data, target.ctypes.data,
+          c.p0, c.R, c.gamma, q.ctypes.data, arrays["D"].ctypes.data,
+          arrays["g"].ctypes.data, arrays["Jinv"].ctypes.data, target.ctypes.data,
           s.cuda_stream)
     return target
 
@@ -355,7 +375,7 @@ def reference_volume_term(state: FieldState,
     builds) take the native host pipeline (``volume_host``)."""
     validate_state(state)
     if all(a.dtype == np.float32 and a.flags.c_contiguous
-           for a in state.arrays().values()):
+           for a in state_arrays(state).values()):
         return volume_host(state, c, compute_dtype=np.float64)
     return volume_term(state, c, dtype=np.float64).astype(np.float32)
 
@@ -366,16 +386,17 @@ def volume_rhs_(state: FieldState, c: PhysicalConstants | None = None, *,
     computed at ``dtype`` (default: the dtype of ``state.rhsq``). Uniform-
     dtype states with the AUTO variant take the native host pipeline."""
     validate_state(state)
-    dt = state.rhsq.dtype if dtype is None else np.dtype(dtype)
-    arrays = state.arrays().values()
-    if variant == "auto" and all(a.dtype == state.rhsq.dtype and a.flags.c_contiguous
-                                 for a in arrays):
+    arrays = state_arrays(state)
+    rhsq = arrays["rhsq"]
+    dt = rhsq.dtype if dtype is None else np.dtype(dtype)
+    if variant == "auto" and all(a.dtype == rhsq.dtype and a.flags.c_contiguous
+                                 for a in arrays.values()):
         volume_host(state, c, accumulate=True, compute_dtype=dt, device=device)
-        return state.rhsq
+        return rhsq
     ds = DeviceFieldState.from_field_state(state, dtype=dt, device=device)
-    volume_rhs_device(ds, variant=variant, constants=c or state.constants)
-    state.rhsq[...] = ds.rhsq_logical().astype(state.rhsq.dtype, copy=False)
-    return state.rhsq
+    volume_rhs_device(ds, variant=variant, constants=c or state_constants(state))
+    rhsq[...] = ds.rhsq_logical().astype(rhsq.dtype, copy=False)
+    return rhsq
 
 
 def interpret_state(kernels, state: FieldState, nq: int, ne: int,
@@ -386,8 +407,7 @@ def interpret_state(kernels, state: FieldState, nq: int, ne: int,
     no interpreter environment). ``kernels`` is accepted for signature
     compatibility and ignored — the CUDA kernel IS the fused kernel."""
     validate_state(state, nq, ne, dtype=np.float32)
-    volume_rhs_(state, dtype=np.float32)
-    return state.rhsq, []
+    return volume_rhs_(state, dtype=np.float32), []
 
 
 def max_rel_error(got: np.ndarray, want: np.ndarray) -> float:

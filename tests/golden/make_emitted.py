@@ -40,7 +40,7 @@ from loopforge.codegen import emit_source  # noqa: E402
 from loopforge.schedule import linearize  # noqa: E402
 
 OUT = pathlib.Path(__file__).resolve().parents[2] / "paper_1604_08501_b200" / "corpus"
-NQS = (2, 4, 8)
+NQS = (2, 3, 4, 8)  # 2, 3, 4: the criterion-1 grid (pkg/tests/test_acceptance.py:65-83)
 
 
 def main() -> None:

@@ -40,7 +40,10 @@ OUT = pathlib.Path(__file__).parent
 
 FULL = [(2, 1, 42), (2, 3, 1), (3, 2, 2), (3, 5, 3), (4, 5, 3), (4, 2, 6),
         (5, 2, 4), (6, 2, 7), (7, 2, 8), (8, 3, 1), (9, 1, 2), (10, 1, 3),
-        (11, 1, 4), (12, 2, 5)]
+        (11, 1, 4), (12, 2, 5),
+        # BASELINE config 1 (C1): stored in full AND hashed, so the GPU
+        # parity tests pin the reference's own output for it
+        (4, 512, 1)]
 HASHED = [(4, 512, 1), (8, 64, 1), (8, 32, 11)]
 INTERP = [(2, 1, 1), (2, 5, 2), (3, 2, 3), (4, 2, 1)]
 
@@ -52,7 +55,7 @@ def sha(a: np.ndarray) -> str:
 def main() -> None:
     arrays: dict[str, np.ndarray] = {}
     meta: dict = {"full": [], "hashed": {}, "interp8": [], "inputs_sha256": {}}
-    for nq, ne, seed in FULL + HASHED:
+    for nq, ne, seed in FULL + [h for h in HASHED if h not in FULL]:
         st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=seed))
         key = f"{nq}_{ne}_{seed}"
         meta["inputs_sha256"][key] = {n: sha(a) for n, a in st.arrays().items()}
@@ -60,7 +63,7 @@ def main() -> None:
         if (nq, ne, seed) in FULL:
             arrays[f"ref_{key}"] = out
             meta["full"].append([nq, ne, seed])
-        else:
+        if (nq, ne, seed) in HASHED:
             meta["hashed"][key] = sha(out)
     for nq, ne, seed in INTERP:
         staged = build_levels(nq, up_to=8)

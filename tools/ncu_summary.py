@@ -95,9 +95,17 @@ def main() -> None:
     if args.out:
         pathlib.Path(args.out).write_text(text + "\n")
     if args.key and ks and "dram_traffic_bytes" in ks[-1]:
+        # stamped with the kernel's source hash: bench.py reports the number
+        # only while the kernel source is unchanged
+        import sys
+        sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+        from bench import kernel_source_sha
+        variant, nq, dtype = args.key.split("|")
         p = pathlib.Path(args.traffic_json)
         doc = json.loads(p.read_text()) if p.exists() else {}
-        doc[args.key] = ks[-1]["dram_traffic_bytes"]
+        doc[args.key] = {"bytes": ks[-1]["dram_traffic_bytes"],
+                         "source_sha": kernel_source_sha(variant, dtype, int(nq.split("=")[1])),
+                         "file": args.out or args.report}
         p.write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
 
 
