@@ -80,6 +80,9 @@ struct LtCfg {
   static constexpr int JOBS = 2 * NT;                // S and T line' tiles
   static constexpr int JPW = (JOBS + W - 1) / W;     // GEMM jobs per warp
   static constexpr int THREADS = 32 * W;
+  // CTAs per SM the registers are budgeted for: one element per CTA, so the
+  // small-Nq instances (4..8 warps) run several CTAs per SM
+  static constexpr int MINB = NQ >= 9 ? 1 : NQ >= 7 ? 2 : 3;
   static constexpr int ROWS = 4 * KS;                // tile rows (rows >= NQ stay zero)
   // row stride (doubles) and swizzle, from the bank model (tools/lt_banks.py)
   // (a multiple of 16 doubles: the swizzle permutes units within 128-byte
@@ -109,7 +112,7 @@ __device__ __forceinline__ int lt_pos(int n, int x) {
 }
 
 template <int NQ, int RPW>
-__global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, 1)
+__global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
     volume_lt_kernel(int64_t ne, double p0, double R, double gam, const double *__restrict__ q,
                      double *__restrict__ rhsq, const double *__restrict__ D,
                      const double *__restrict__ g, const double *__restrict__ jinv) {
@@ -468,7 +471,13 @@ int launch_lt(int64_t ne, double p0, double R, double gam, const double *q, doub
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return LFB_ERR_CUDA;
-  const int64_t grid = ne < sms ? ne : sms;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return LFB_ERR_LAUNCH;
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;
   kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
   LFB_CHECK_LAUNCH();
@@ -477,12 +486,16 @@ int launch_lt(int64_t ne, double p0, double R, double gam, const double *q, doub
 
 }  // namespace
 
-bool lt_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq >= 9 && nq <= 12; }
+bool lt_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq >= 5 && nq <= 12; }
 
 int volume_lt_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
                   double *rhsq, const double *D, const double *g, const double *jinv,
                   cudaStream_t s) {
   switch (nq) {
+    case 5: return launch_lt<5, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 6: return launch_lt<6, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 7: return launch_lt<7, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 8: return launch_lt<8, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
     case 9: return launch_lt<9, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
     case 10: return launch_lt<10, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
     case 11: return launch_lt<11, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
