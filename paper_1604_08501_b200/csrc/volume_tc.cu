@@ -41,6 +41,7 @@
 #include "lfb_common.cuh"
 #include "lfb_math.cuh"
 
+
 namespace lfb {
 
 int volume_basic_f64(int, int64_t, double, double, double, const double *, double *,
@@ -167,12 +168,16 @@ constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
 constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
 
-template <typename T, int NS>
+// NW < 8 (zero-padded Nq, one warp per real k-plane): stages hold the real
+// q + g slab only (+ the g superset's 16-byte shift)
+template <typename T, int NS, int SUB, int NW>
 struct TcSmem {
-  T stage[NS][tc_stage_alloc<T>()];
+  static constexpr int STAGE =
+      NW == 8 ? tc_stage_alloc<T>() : ((17 * SUB * SUB * SUB + 2 + 1) & ~1);
+  T stage[NS][STAGE];
   double ft[8 * FT_FS];
   double tout[8 * TO_FS];
-  double stile[TC_WARPS][2][ST_SZ];
+  double stile[NW][2][ST_SZ];
   unsigned long long bar[NS];
 };
 
@@ -212,13 +217,16 @@ __device__ __forceinline__ void sts2(double *p, double a, double b) {
 // (tests/test_mutants.py; cf. the reference's barrier-deletion mutation test,
 // pkg/tests/test_acceptance.py:191-219): 1 drops the F_t barrier, 2 the
 // T-out barrier, 3 the per-warp S-tile __syncwarp.
-template <typename T, int NS, int SUB, int MUT = 0>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <typename T, int NS, int SUB, int MUT = 0, int NW = TC_WARPS>
+__global__ void __launch_bounds__(32 * NW, 1)
     volume_tc_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                      T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                      const T *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TcSmem<T, NS> &sm = *reinterpret_cast<TcSmem<T, NS> *>(smem_raw);
+  TcSmem<T, NS, SUB, NW> &sm = *reinterpret_cast<TcSmem<T, NS, SUB, NW> *>(smem_raw);
+  if (NW < 8) {  // F_t planes k >= SUB have no owner warp: they stay zero
+    for (int x = threadIdx.x; x < 8 * FT_FS; x += 32 * NW) sm.ft[x] = 0.0;
+  }
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
@@ -494,24 +502,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // back as soon as its T result is exchanged (no 8-field register state).
 // The next element's TMA is issued when the element is done (its bytes are
 // already L2-prefetched); the co-resident CTA computes meanwhile.
-template <typename T>
-struct TcSmemLean {
-  T stage[TC_STAGE];
-  double ft[8 * FT_FS];
-  unsigned long long bar;
-};
+//
+// PLANE variant (NW = SUB < 8 warps, zero-padded Nq = 5..7): only the SUB
+// real k-planes get a warp (the 8 - SUB all-padding planes of the virtual
+// cube issued DMMAs on zeros), the stage holds just the element's real
+// q + g slab, the padding planes of the F_t tile are zeroed once, and
+// several such CTAs share an SM (MINB).
 constexpr int LEAN_TOUT = 0;                    // doubles into the stage: tout[2][TO_FS]
-constexpr int LEAN_STILE = 2 * TO_FS;           // stile[8 warps][ST_SZ]
-static_assert(LEAN_STILE + TC_WARPS * ST_SZ <= TC_STAGE / 2, "aliases fit in a f32 stage");
+constexpr int LEAN_STILE = 2 * TO_FS;           // stile[NW warps][ST_SZ]
 
-template <typename T, int SUB>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+template <typename T, int SUB, int NW>
+struct TcLeanCfg {
+  static constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
+  // NW = 8: the virtual-cube stage; NW < 8: the real slab (+ the g superset's
+  // 16-byte shift), at least as large as the tout / stile aliases
+  static constexpr int REAL = (17 * SUB * SUB * SUB + 2 + 1) & ~1;
+  static constexpr int ALIAS = (LEAN_STILE + NW * ST_SZ) * (int)(sizeof(double) / sizeof(T));
+  static constexpr int STAGE = NW == 8 ? TC_STAGE : (REAL > ALIAS ? REAL : ALIAS);
+  static constexpr int MINB = NW == 8 ? 2 : (SUB == 5 ? 3 : 2);
+  // NW < 8, Nq <= 6: a 2-stage ring — element n+1's copy is issued when
+  // element n starts (its stage was element n-1's, free after n-1's last
+  // barrier); at Nq = 7 two stages would leave one CTA per SM
+  static constexpr int NSTG = (NW < 8 && SUB <= 6) ? 2 : 1;  // Nq=7: 2 stages -> 1 CTA/SM
+  static_assert(NW == 8 || PAD, "plane variant is for the zero-padded Nq");
+  static_assert(LEAN_STILE + NW * ST_SZ <= STAGE * (int)sizeof(T) / (int)sizeof(double),
+                "aliases fit in the stage");
+};
+
+template <typename T, int SUB, int NW>
+struct TcSmemLean {
+  T stage[TcLeanCfg<T, SUB, NW>::NSTG][TcLeanCfg<T, SUB, NW>::STAGE];
+  double ft[8 * FT_FS];
+  unsigned long long bar[TcLeanCfg<T, SUB, NW>::NSTG];
+};
+
+template <typename T, int SUB, int NW = TC_WARPS>
+__global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
     volume_tc_lean_kernel(int64_t ne, double p0, double R, double gam, const T *__restrict__ q,
                           T *__restrict__ rhsq, const T *__restrict__ D,
                           const T *__restrict__ g, const T *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TcSmemLean<T> &sm = *reinterpret_cast<TcSmemLean<T> *>(smem_raw);
-  double *const alias = reinterpret_cast<double *>(sm.stage);
+  TcSmemLean<T, SUB, NW> &sm = *reinterpret_cast<TcSmemLean<T, SUB, NW> *>(smem_raw);
+  constexpr int NSTG = TcLeanCfg<T, SUB, NW>::NSTG;
+  if (NW < 8) {  // F_t planes k >= SUB have no owner warp: they stay zero
+    for (int x = threadIdx.x; x < 8 * FT_FS; x += 32 * NW) sm.ft[x] = 0.0;
+  }
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
@@ -560,31 +595,40 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     bytes = (uint32_t)(hi - lo);
   };
 
-  uint64_t *bar = reinterpret_cast<uint64_t *>(&sm.bar);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm.bar);
   if (tid == 0) {
-    mbar_init(bar, 1);
+#pragma unroll
+    for (int x = 0; x < NSTG; ++x) mbar_init(&bars[x], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int64_t n) {
     const int64_t e = e0 + n * G;
+    const int st = (int)(n % NSTG);
     const T *gs;
     uint32_t gb;
     span16(g + e * SLABG, SLABG, gs, gb);
-    mbar_expect_tx(bar, SLABQ * sizeof(T) + gb);
-    bulk_g2s(sm.stage, q + e * SLABQ, SLABQ * sizeof(T), bar);
-    bulk_g2s(sm.stage + SLABQ, gs, gb, bar);
+    mbar_expect_tx(&bars[st], SLABQ * sizeof(T) + gb);
+    bulk_g2s(sm.stage[st], q + e * SLABQ, SLABQ * sizeof(T), &bars[st]);
+    bulk_g2s(sm.stage[st] + SLABQ, gs, gb, &bars[st]);
   };
   if (tid == 0 && nmine > 0) issue(0);
 
   for (int64_t n = 0; n < nmine; ++n) {
     const int64_t e = e0 + n * G;
-    // L2 prefetch of the next element (its TMA is issued at the end of this one)
+    const int st = (int)(n % NSTG);
+    double *const alias = reinterpret_cast<double *>(sm.stage[st]);
+    if (NSTG == 2 && tid == 0 && n + 1 < nmine) {
+      fence_proxy_async();  // the other stage's last reads were before the previous barrier
+      issue(n + 1);
+    }
+    // L2 prefetch of the next element (NSTG = 1: its q / g TMA is issued at
+    // the end of this one; NSTG = 2: already issued above)
     if (n + 1 < nmine) {
       const int64_t en = e + G;
       const T *sp;
       uint32_t sb_;
-      if (tid == 0) {
+      if (NSTG == 1 && tid == 0) {
         prefetch_l2(q + en * SLABQ, SLABQ * sizeof(T));
         span16(g + en * SLABG, SLABG, sp, sb_);
         prefetch_l2(sp, sb_);
@@ -594,8 +638,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         prefetch_l2(sp, sb_);
       }
     }
-    const T *sq = sm.stage;
-    const T *sg = sm.stage + SLABQ +
+    const T *sq = sm.stage[st];
+    const T *sg = sm.stage[st] + SLABQ +
                   (PAD ? (reinterpret_cast<uintptr_t>(g + e * SLABG) & 15) / sizeof(T) : 0);
     T *re = rhsq + e * SLABQ;
     double jv[2];
@@ -606,7 +650,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       ldg_pair(jinv + e * SLABJ + jo, jv[0], jv[1]);
     }
 
-    mbar_wait(bar, (uint32_t)(n & 1));
+    mbar_wait(&bars[st], (uint32_t)((n / NSTG) & 1));
 
     // ---- phase 1 (as in the 1-CTA kernel) ----------------------------------
     double sb[8][2], V0[2], V1[2], pP[2], gr[3][2], gs[3][2];
@@ -715,32 +759,32 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       }
     }
     __syncthreads();  // every alias read done: the stage may be refilled
-    if (tid == 0 && n + 1 < nmine) {
+    if (NSTG == 1 && tid == 0 && n + 1 < nmine) {
       fence_proxy_async();
       issue(n + 1);
     }
   }
 }
 
-template <typename T, int SUB>
+template <typename T, int SUB, int NW = TC_WARPS>
 int launch_tc_lean(int64_t ngroups, double p0, double R, double gam, const T *q, T *rhsq,
                    const T *D, const T *g, const T *jinv, cudaStream_t stream) {
-  const size_t smem = sizeof(TcSmemLean<T>);
-  auto kern = volume_tc_lean_kernel<T, SUB>;
+  const size_t smem = sizeof(TcSmemLean<T, SUB, NW>);
+  auto kern = volume_tc_lean_kernel<T, SUB, NW>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, smem) !=
           cudaSuccess)
     return LFB_ERR_CUDA;
   if (per_sm < 1) return LFB_ERR_LAUNCH;
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t grid = ngroups < slots ? ngroups : slots;
   if (grid == 0) return LFB_OK;
-  kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
+  kern<<<(unsigned)grid, 32 * NW, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
   LFB_CHECK_LAUNCH();
   return LFB_OK;
 }
@@ -754,12 +798,17 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
   // further 2-CTA schedules for Nq=8 — q staged, g from L2; q and g staged,
   // T-out in the dead stage — lost to the ring, profiles/r01_ab_qstage.txt,
   // r01_ab_qg.txt, and were removed.)
+  // Zero-padded Nq = 5..7: the LEAN schedule with one warp per real
+  // k-plane (PLANE variant; vs 8 warps: Nq=5 0.49 / 0.34, Nq=6 0.62 / 0.51,
+  // Nq=7 0.72 / 0.70 of HBM; the 1-CTA ring with SUB warps: 0.31 / 0.51 /
+  // 0.67 — profiles/r02_tc_plane.txt)
   constexpr bool PAD_ = !(SUB == 8 || SUB == 4 || SUB == 2);
   if constexpr (PAD_) {
-    return launch_tc_lean<T, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
+    return launch_tc_lean<T, SUB, SUB>(ngroups, p0, R, gam, q, rhsq, D, g, jinv, stream);
   } else {
-    const size_t smem = sizeof(TcSmem<T, NS>);
-    auto kern = volume_tc_kernel<T, NS, SUB>;
+    constexpr int NW = TC_WARPS;
+    const size_t smem = sizeof(TcSmem<T, NS, SUB, NW>);
+    auto kern = volume_tc_kernel<T, NS, SUB, 0, NW>;
 #ifdef LFB_EXPERIMENTS
     // barrier-deletion mutants for the race-detector test (tests/test_mutants.py),
     // built only into the test library liblfb_volume_mutants.so
@@ -778,7 +827,7 @@ int launch_tc(int64_t ngroups, double p0, double R, double gam, const T *q, T *r
       return LFB_ERR_CUDA;
     const int64_t grid = ngroups < sms ? ngroups : sms;
     if (grid == 0) return LFB_OK;
-    kern<<<(unsigned)grid, TC_THREADS, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
+    kern<<<(unsigned)grid, 32 * NW, smem, stream>>>(ngroups, p0, R, gam, q, rhsq, D, g, jinv);
     LFB_CHECK_LAUNCH();
     return LFB_OK;
   }
