@@ -32,6 +32,8 @@ bool lines_available(int dtype_bytes, int nq);
 int volume_lt_f64(int, int64_t, double, double, double, const double *, double *,
                   const double *, const double *, const double *, cudaStream_t);
 bool lt_available(int dtype_bytes, int nq);
+int volume_lt_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                  const float *, const float *, cudaStream_t);
 int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
                    const double *, const double *, const double *, cudaStream_t);
 int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
@@ -64,18 +66,21 @@ int validate(int nq, int64_t ne, T p0, T R, T gam, const T *q, const T *rhsq,
 
 int resolve(int variant, int bytes, int nq) {
   if (variant == LFB_VARIANT_AUTO) {
-    // measured on B200 (profiles/r01_sweep_*.jsonl, profiles/r01_col_sweep_*.jsonl):
+    // measured on B200 (profiles/r01_sweep_*.jsonl, profiles/r01_col_sweep_*.jsonl,
+    // profiles/r02_*):
     // col wins where tc pads most of its virtual Nq=8 cube (Nq 5, 6) and
     // for fp32 above Nq = 8 (FFMA vs the fp64 DMMA line GEMMs); tc keeps
     // Nq 2, 4, 7, 8 and fp32 Nq 13..16 (the 16x16-plane TF32 kernel); lines
     // keeps fp64 Nq 9..13 (profiles/r01_col_configs.txt, r01_tc16.txt)
+    // line tiles (volume_lt*.cu) where they lead: Nq 11, 12 in both
+    // precisions (round 2, profiles/r02_sweep_*.jsonl)
+    if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::col_available(bytes, nq)) {
       if (nq == 5 || nq == 6) return LFB_VARIANT_COL;
       if (bytes == 4 && nq >= 9 && nq <= 12) return LFB_VARIANT_COL;
       if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }
     if (lfb::tc_available(bytes, nq)) return LFB_VARIANT_TC;
-    if (bytes == 8 && nq == 12 && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::lines_available(bytes, nq)) return LFB_VARIANT_LINES;
     return lfb::fused_available(bytes, nq) ? LFB_VARIANT_FUSED : LFB_VARIANT_BASIC;
   }
@@ -144,7 +149,8 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
       if (!lfb::lines_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lines_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_LT:
-      return LFB_ERR_BAD_VARIANT;
+      if (!lfb::lt_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lt_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_COL:
       if (!lfb::col_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);

@@ -132,12 +132,6 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int gq = lane >> 2, c = lane & 3;
   const double Rp0 = R / p0;
-  // the bulk copies take whole 16-byte units; the last unit of an array may
-  // be half outside it, so values at or beyond its tail are read from global
-  auto tail_of = [](const double *end) {
-    return reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(end) & ~(uintptr_t)15);
-  };
-  const double *gtail = tail_of(g + ne * 9 * NPT), *qtail = tail_of(q + ne * 8 * NPT);
 
   for (int x = tid; x < 8 * TILE; x += C::THREADS) lt_sm[x] = 0.0;
   if (tid == 0) {
@@ -204,10 +198,8 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
     for (int x = 0; x < 4; ++x) {
       if (x > 0 && !mom) break;
       const double *a0 = x == 0 ? q + (e * 8 + b) * NPT : g + (e * 9 + 3 * (x - 1) + b - 1) * NPT;
-      const double *tl = x == 0 ? qtail : gtail;
       const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15;
       uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + NPT) + 15) & ~(uintptr_t)15;
-      if (hi > reinterpret_cast<uintptr_t>(tl)) hi = reinterpret_cast<uintptr_t>(tl);
       src[x] = reinterpret_cast<const double *>(lo);
       bytes[x] = (uint32_t)(hi - lo);
       total += bytes[x];
@@ -228,9 +220,11 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   // every other element reads shared memory unconditionally (a predicated
   // global fallback in the hot path would hold a long scoreboard on the
   // destination register even when no lane takes it).
-  auto staged = [](const double *a0, const double *st, const double *tl, int o, bool last) {
+  // value o of a slab starting at global a0, from its stage copy st (the
+  // copy starts at the 16-byte unit below a0; the launcher never hands this
+  // kernel an element whose aligned superset would leave the arrays)
+  auto staged = [](const double *a0, const double *st, int o) {
     const int sh = (NPT & 1) ? (int)((reinterpret_cast<uintptr_t>(a0) & 15) >> 3) : 0;
-    if ((NPT & 1) && last) return a0 + o < tl ? st[sh + o] : __ldg(a0 + o);
     return st[sh + o];
   };
 
@@ -306,7 +300,6 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
     const double *qe = q + e * 8 * NPT + c;
     const double *ge = g + e * 9 * NPT + c;
     double *re = rhsq + e * 8 * NPT + c;
-    const bool lastel = e == ne - 1;
     const int64_t en = e + gridDim.x;
     if (LT_PF == 1 && tid == 32 && en < ne) {
       // next element's phase-1 inputs into L2: rho, U, Theta, g, Jinv
@@ -387,14 +380,13 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
             const int o = pofs[m] + c + 4 * t;  // point index in the slab
-            const double qv = vt[m][t] ? staged(qslab, st, qtail, o, lastel) : 0.0;
+            const double qv = vt[m][t] ? staged(qslab, st, o) : 0.0;
             double fr = Wd[0][m][t] * qv, fs = Wd[1][m][t] * qv, ft = Wd[2][m][t] * qv;
             if (mom && vt[m][t]) {
               double gd[3];
 #pragma unroll
               for (int d = 0; d < 3; ++d)
-                gd[d] = staged(g + (e * 9 + 3 * d + f - 1) * NPT, st + (1 + d) * GSLAB, gtail,
-                               o, lastel);
+                gd[d] = staged(g + (e * 9 + 3 * d + f - 1) * NPT, st + (1 + d) * GSLAB, o);
               fr = fma(gd[0], pp[m][t], fr);
               fs = fma(gd[1], pp[m][t], fs);
               ft = fma(gd[2], pp[m][t], ft);
@@ -486,11 +478,18 @@ int launch_lt(int64_t ne, double p0, double R, double gam, const double *q, doub
 
 }  // namespace
 
-bool lt_available(int dtype_bytes, int nq) { return dtype_bytes == 8 && nq >= 5 && nq <= 12; }
+bool lt32_available(int nq);
+bool lt_available(int dtype_bytes, int nq) {
+  return dtype_bytes == 8 ? (nq >= 5 && nq <= 12) : (dtype_bytes == 4 && lt32_available(nq));
+}
 
-int volume_lt_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
-                  double *rhsq, const double *D, const double *g, const double *jinv,
-                  cudaStream_t s) {
+int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
+                   const double *, const double *, const double *, cudaStream_t);
+
+namespace {
+int dispatch_lt(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                double *rhsq, const double *D, const double *g, const double *jinv,
+                cudaStream_t s) {
   switch (nq) {
     case 5: return launch_lt<5, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
     case 6: return launch_lt<6, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
@@ -502,6 +501,24 @@ int volume_lt_f64(int nq, int64_t ne, double p0, double R, double gam, const dou
     case 12: return launch_lt<12, LT_RPW>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
     default: return LFB_ERR_BAD_VARIANT;
   }
+}
+}  // namespace
+
+// The bulk copies need 16-byte aligned q / g (else: the column kernel). For
+// odd Nq a slab is not a 16-byte multiple and the last element — whose
+// aligned superset would leave the arrays — goes to the column kernel.
+int volume_lt_f64(int nq, int64_t ne, double p0, double R, double gam, const double *q,
+                  double *rhsq, const double *D, const double *g, const double *jinv,
+                  cudaStream_t s) {
+  if (!lt_available(8, nq)) return LFB_ERR_BAD_VARIANT;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(g)) & 15)
+    return volume_col_f64(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  const int64_t npt = (int64_t)nq * nq * nq;
+  const int64_t n = ((npt * 8) % 16 && ne > 0) ? ne - 1 : ne;
+  int rc = n > 0 ? dispatch_lt(nq, n, p0, R, gam, q, rhsq, D, g, jinv, s) : LFB_OK;
+  if (rc != LFB_OK || n == ne) return rc;
+  return volume_col_f64(nq, ne - n, p0, R, gam, q + n * 8 * npt, rhsq + n * 8 * npt, D,
+                        g + n * 9 * npt, jinv + n * npt, s);
 }
 
 }  // namespace lfb
