@@ -84,31 +84,34 @@ struct LtCfg {
   // small-Nq instances (4..8 warps) run several CTAs per SM
   static constexpr int MINB = NQ >= 9 ? 1 : NQ >= 7 ? 2 : 3;
   static constexpr int ROWS = 4 * KS;                // tile rows (rows >= NQ stay zero)
-  // row stride (doubles) and swizzle, from the bank model (tools/lt_banks.py)
-  // (a multiple of 16 doubles: the swizzle permutes units within 128-byte
-  // segments, so a row must consist of whole segments)
-  static constexpr int RS = (NT * 8 + 15) / 16 * 16;
+  // row stride (doubles): the line' range plus the largest row offset of
+  // lt_pos, in whole 128-byte segments (bank model: tools/lt_banks.py)
+  static constexpr int RS = (NT * 8 + 12 + 15) / 16 * 16;
   static constexpr int TILE = ROWS * RS;
   static_assert(RS >= NT * 8, "row holds every line' tile");
   // field stage slab: a 16-byte aligned superset of one Nq^3 slab
   static constexpr int GSLAB = (NPT + 3) & ~1;
-  // 2 bufs x {fS, fT, cS, cT} tiles + 2 field stages x {q_b, g(b-1, 0..2)}
-  // slabs + 2 mbarriers
+  // 2 bufs x {fS, fT, cS, cT} tiles + 2 q stages + 1 g stage (3 slabs) +
+  // 3 mbarriers
   // + the per-lane D fragment tables (R: NTL x KS, S/T: MT x KS values per lane)
   static constexpr int DTAB = (NTL + MT) * KS * 32;
   static constexpr size_t SMEM =
-      sizeof(double) * (8 * (size_t)TILE + 8 * (size_t)GSLAB + DTAB + 2);
+      sizeof(double) * (8 * (size_t)TILE + 5 * (size_t)GSLAB + DTAB + 3);
 };
 
-// position of X[n][x] in a tile: the 16-byte unit of x is XOR-swizzled within
-// its 128-byte row segment by a function of the row
+// position of X[n][x] in a tile: row n starts 8 (n&1) + 4 ((n>>1)&1) doubles
+// into its 128-byte segment, so four consecutive rows (a B fragment, an
+// owner access) and two consecutive rows of 16-byte pairs (a C fragment) hit
+// distinct bank groups; linear in x, so a lane's own points are base + 4t
+// field processed at pipeline position p: the momentum fields (which also
+// need the g(b-1, .) stage) on positions 0, 2, 4, so one g stage suffices
+__device__ __forceinline__ int lt_field(int p) {
+  return (p & 1) ? (p == 7 ? 7 : 4 + (p >> 1)) : (p == 6 ? 0 : 1 + (p >> 1));
+}
+
 template <int NQ>
 __device__ __forceinline__ int lt_pos(int n, int x) {
-  using C = LtCfg<NQ, 1>;
-  const int h = 4 * (n & 1) + 2 * ((n >> 1) & 1);
-  const int u = x >> 1;
-  const int pu = (u & ~7) | ((u ^ h) & 7);
-  return n * C::RS + 2 * pu + (x & 1);
+  return n * LtCfg<NQ, 1>::RS + 8 * (n & 1) + 4 * ((n >> 1) & 1) + x;
 }
 
 template <int NQ, int RPW>
@@ -122,12 +125,14 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   extern __shared__ __align__(16) double lt_sm[];
   // tile (buffer b&1, kind): 0 F_s, 1 F_t, 2 C_s, 3 C_t
   auto tile = [&](int buf, int kind) { return lt_sm + (buf * 4 + kind) * TILE; };
-  // field stage (buffer b&1): slab 0 = q_b, slabs 1..3 = g(b-1, d) of a
-  // momentum field b = 1..3, all bulk-copied two fields ahead
-  double *fst = lt_sm + 8 * TILE;
+  // q stages [2][GSLAB] (the field at position p, bulk-copied two regions
+  // ahead) and ONE g stage [3][GSLAB] (g(b-1, d) of the momentum fields,
+  // which sit at positions 0, 2, 4 — lt_field — one region ahead)
+  double *qst = lt_sm + 8 * TILE;
+  double *gst = qst + 2 * GSLAB;
   // D fragments, one value per lane: brt[(u*KS + t)*32 + lane], adt[(mt*KS + t)*32 + lane]
-  double *brt = fst + 2 * 4 * GSLAB, *adt = brt + NTL * KS * 32;
-  uint64_t *fbar = reinterpret_cast<uint64_t *>(brt + C::DTAB);
+  double *brt = gst + 3 * GSLAB, *adt = brt + NTL * KS * 32;
+  uint64_t *fbar = reinterpret_cast<uint64_t *>(brt + C::DTAB);  // q0, q1, g
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int gq = lane >> 2, c = lane & 3;
@@ -137,6 +142,7 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   if (tid == 0) {
     mbar_init(&fbar[0], 1);
     mbar_init(&fbar[1], 1);
+    mbar_init(&fbar[2], 1);
     mbar_init_fence();
   }
 
@@ -153,15 +159,16 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
 #pragma unroll
     for (int t = 0; t < KS; ++t) vt[m][t] = own && c + 4 * t < NQ;
   }
-  // smem positions of own point (m, t) in the S and T layouts
-  auto posS = [&](int m, int t) {
+  // smem positions of own point (m, t) in the S and T layouts: base + 4t
+  int sS0[RPW], sT0[RPW];
+#pragma unroll
+  for (int m = 0; m < RPW; ++m) {
     const int L = 8 * (RPW * w + m) + gq, jj = L % C::LPJ, kk = L / C::LPJ;
-    return lt_pos<NQ>(jj, kk * LP + c + 4 * t);
-  };
-  auto posT = [&](int m, int t) {
-    const int L = 8 * (RPW * w + m) + gq, jj = L % C::LPJ, kk = L / C::LPJ;
-    return lt_pos<NQ>(kk, jj * LP + c + 4 * t);
-  };
+    sS0[m] = lt_pos<NQ>(jj, kk * LP + c);
+    sT0[m] = lt_pos<NQ>(kk, jj * LP + c);
+  }
+  auto posS = [&](int m, int t) { return sS0[m] + 4 * t; };
+  auto posT = [&](int m, int t) { return sT0[m] + 4 * t; };
   // ---- D fragments (D[n*NQ + i] = D(i, n)) --------------------------------
   //   R: B[k-row c][n-col g] at step t = D(out = slot(u, g), n = c + 4t),
   //      slot(u, x) = c' + 4(2u + s') for x = 2c' + s';
@@ -186,40 +193,34 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   }
   __syncthreads();
 
-  // field b of element e into stage buffer b & 1 (thread 0): q_b and, for a
-  // momentum field, g(b-1, d), d = 0..2 — each the 16-byte aligned superset
-  // of its slab, clipped at the array's tail
-  auto issue_field = [&](int64_t e, int b) {
-    uint64_t *bar = &fbar[b & 1];
-    const bool mom = b >= 1 && b <= 3;
-    const double *src[4];
-    uint32_t bytes[4], total = 0;
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      if (x > 0 && !mom) break;
-      const double *a0 = x == 0 ? q + (e * 8 + b) * NPT : g + (e * 9 + 3 * (x - 1) + b - 1) * NPT;
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15;
-      uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + NPT) + 15) & ~(uintptr_t)15;
-      src[x] = reinterpret_cast<const double *>(lo);
-      bytes[x] = (uint32_t)(hi - lo);
-      total += bytes[x];
-    }
-    mbar_expect_tx(bar, total);
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      if (x > 0 && !mom) break;
-      if (LT_HINT)
-        bulk_g2s_hint(fst + ((b & 1) * 4 + x) * GSLAB, src[x], bytes[x], bar,
-                      l2_evict_first_policy());
-      else
-        bulk_g2s(fst + ((b & 1) * 4 + x) * GSLAB, src[x], bytes[x], bar);
-    }
+  // bulk copies (thread 0) of a slab's 16-byte aligned superset (the
+  // launcher never hands this kernel an element whose superset would leave
+  // the arrays)
+  auto slab_bytes = [&](const double *a0) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + NPT) + 15) & ~(uintptr_t)15;
+    return (uint32_t)(hi - lo);
   };
-  // value o of a slab starting at global a0, from its stage copy st. Only
-  // the last element of an odd-Nq array can reach the clipped tail unit, so
-  // every other element reads shared memory unconditionally (a predicated
-  // global fallback in the hot path would hold a long scoreboard on the
-  // destination register even when no lane takes it).
+  auto slab_copy = [&](double *dst, const double *a0, uint64_t *bar) {
+    const void *src = reinterpret_cast<const void *>(reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15);
+    if (LT_HINT)
+      bulk_g2s_hint(dst, src, slab_bytes(a0), bar, l2_evict_first_policy());
+    else
+      bulk_g2s(dst, src, slab_bytes(a0), bar);
+  };
+  auto issue_q = [&](int64_t e, int p) {  // q of the field at position p -> q stage p & 1
+    const double *a0 = q + (e * 8 + lt_field(p)) * NPT;
+    mbar_expect_tx(&fbar[p & 1], slab_bytes(a0));
+    slab_copy(qst + (p & 1) * GSLAB, a0, &fbar[p & 1]);
+  };
+  auto issue_g = [&](int64_t e, int b) {  // g(b-1, d), d = 0..2 -> the g stage
+    uint32_t total = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) total += slab_bytes(g + (e * 9 + 3 * d + b - 1) * NPT);
+    mbar_expect_tx(&fbar[2], total);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) slab_copy(gst + d * GSLAB, g + (e * 9 + 3 * d + b - 1) * NPT, &fbar[2]);
+  };
   // value o of a slab starting at global a0, from its stage copy st (the
   // copy starts at the 16-byte unit below a0; the launcher never hands this
   // kernel an element whose aligned superset would leave the arrays)
@@ -282,9 +283,11 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
 
   int64_t e = blockIdx.x;
   if (tid == 0 && e < ne) {
-    issue_field(e, 0);
-    issue_field(e, 1);
+    issue_q(e, 0);
+    issue_q(e, 1);
+    issue_g(e, lt_field(0));
   }
+  uint32_t gpar = 0;
   double part[2][RPW][KS];  // rhsq_f + Jinv R_f of fields f-1, f-2 (by f & 1)
   double rhn[RPW][KS];      // rhsq of the next field, loaded one region ahead
   if (e < ne) {
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
     for (int m = 0; m < RPW; ++m)
 #pragma unroll
       for (int t = 0; t < KS; ++t)
-        rhn[m][t] = vt[m][t] ? rhsq[e * 8 * NPT + c + pofs[m] + 4 * t] : 0.0;
+        rhn[m][t] = vt[m][t] ? rhsq[(e * 8 + lt_field(0)) * NPT + c + pofs[m] + 4 * t] : 0.0;
   }
   double jvp[RPW][KS];      // Jinv of the previous element (its fields 6, 7)
   double *rep = nullptr;    // rhsq + c of the previous element
@@ -347,12 +350,14 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
 #pragma unroll
     for (int f = 0; f < 8; ++f) {
       // ---- A: fluxes of field f, R contraction ------------------------------
-      const bool mom = f >= 1 && f <= 3;  // momentum field: pressure term g(f-1, d) p
+      const int b = lt_field(f);            // the field at position f
+      const bool mom = b >= 1 && b <= 3;  // momentum field: pressure term g(b-1, d) p
       // rhsq of field f arrived during region f-1; issue field f+1's (the next
       // element's field 0 after f = 7) and pull field f+2's slab into L2
       double rh[RPW][KS];
       {
-        double *rnext = f < 7 ? re + (f + 1) * NPT : rhsq + en * 8 * NPT + c;
+        const int bn = lt_field((f + 1) & 7);
+        double *rnext = f < 7 ? re + bn * NPT : rhsq + (en * 8 + bn) * NPT + c;
         const bool have = f < 7 || en < ne;
 #pragma unroll
         for (int m = 0; m < RPW; ++m)
@@ -363,17 +368,21 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
           }
         if (tid == 64) {
           if (f + 2 < 8)
-            prefetch_l2_range(rhsq + (e * 8 + f + 2) * NPT, (uint64_t)NPT * sizeof(double));
+            prefetch_l2_range(rhsq + (e * 8 + lt_field(f + 2)) * NPT, (uint64_t)NPT * sizeof(double));
           else if (en < ne)
-            prefetch_l2_range(rhsq + (en * 8 + f - 6) * NPT, (uint64_t)NPT * sizeof(double));
+            prefetch_l2_range(rhsq + (en * 8 + lt_field(f - 6)) * NPT, (uint64_t)NPT * sizeof(double));
         }
       }
       mbar_wait(&fbar[f & 1], (uint32_t)((f >> 1) & 1));  // 4 fills per buffer per element
+      if (mom) {
+        mbar_wait(&fbar[2], gpar);
+        gpar ^= 1u;
+      }
       double pnew[RPW][KS];  // part of field f (slot f & 1 still holds field f-2)
       {
         double *fS = tile(f & 1, 0), *fT = tile(f & 1, 1);
-        const double *st = fst + (f & 1) * 4 * GSLAB;
-        const double *qslab = q + (e * 8 + f) * NPT;
+        const double *st = qst + (f & 1) * GSLAB;
+        const double *qslab = q + (e * 8 + b) * NPT;
 #pragma unroll
         for (int m = 0; m < RPW; ++m) {
           double Fr[KS];
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
               double gd[3];
 #pragma unroll
               for (int d = 0; d < 3; ++d)
-                gd[d] = staged(g + (e * 9 + 3 * d + f - 1) * NPT, st + (1 + d) * GSLAB, o);
+                gd[d] = staged(g + (e * 9 + 3 * d + b - 1) * NPT, gst + d * GSLAB, o);
               fr = fma(gd[0], pp[m][t], fr);
               fs = fma(gd[1], pp[m][t], fs);
               ft = fma(gd[2], pp[m][t], ft);
@@ -414,8 +423,8 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
       // ---- B: S/T GEMMs of the previous field --------------------------------
       if (f >= 1 || rep != nullptr) gemm_st((f + 1) & 1);
       // ---- C: combine the field before that ---------------------------------
-      if (f >= 2) combine(f & 1, re + (f - 2) * NPT, part[f & 1], jv);
-      else if (rep != nullptr) combine(f & 1, rep + (6 + f) * NPT, part[f & 1], jvp);
+      if (f >= 2) combine(f & 1, re + lt_field(f - 2) * NPT, part[f & 1], jv);
+      else if (rep != nullptr) combine(f & 1, rep + lt_field(6 + f) * NPT, part[f & 1], jvp);
 #pragma unroll
       for (int m = 0; m < RPW; ++m)
 #pragma unroll
@@ -426,14 +435,12 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
         prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(double));
       }
       __syncthreads();
-      if (tid == 0) {  // stage of field f+2 (or the next element's fields 0, 1)
-        if (f + 2 < 8) {
-          fence_proxy_async();
-          issue_field(e, f + 2);
-        } else if (en < ne) {
-          fence_proxy_async();
-          issue_field(en, f - 6);
-        }
+      if (tid == 0) {  // q stage of position f+2 (or the next element's 0, 1), g stages
+        fence_proxy_async();
+        if (f + 2 < 8) issue_q(e, f + 2);
+        else if (en < ne) issue_q(en, f - 6);
+        if (f == 0 || f == 2) issue_g(e, lt_field(f + 2));
+        else if (f == 4 && en < ne) issue_g(en, lt_field(0));
       }
     }
 #pragma unroll
@@ -445,9 +452,9 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
   // ---- drain: GEMMs of the last field, combine of the last two ------------
   if (rep != nullptr) {
     gemm_st(1);
-    combine(0, rep + 6 * NPT, part[0], jvp);
+    combine(0, rep + lt_field(6) * NPT, part[0], jvp);
     __syncthreads();
-    combine(1, rep + 7 * NPT, part[1], jvp);
+    combine(1, rep + lt_field(7) * NPT, part[1], jvp);
   }
 }
 
