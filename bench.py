@@ -65,6 +65,7 @@ KERNEL_SOURCES = {
     "col": ("volume_col.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "lines": ("volume_lines.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "lt": ("volume_lt.cu", "lfb_common.cuh", "lfb_math.cuh", "lfb_tma.cuh"),
+    "lt32": ("volume_lt32.cu", "lfb_common.cuh", "lfb_tma.cuh"),
     "fused": ("volume_fused.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "basic": ("volume_basic.cu", "lfb_common.cuh"),
 }
@@ -76,6 +77,8 @@ def kernel_source_sha(variant: str, dtype: str, nq: int) -> str | None:
     name = variant
     if variant == "tc" and dtype == "f32":
         name = "tc16" if nq >= 9 else "tc32"
+    if variant == "lt" and dtype == "f32":
+        name = "lt32"
     files = KERNEL_SOURCES.get(name)
     if not files:
         return None
