@@ -7,11 +7,11 @@ mkdir -p gpurun_out
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.txt 2>&1
-timeout 900 python bench.py --e2e-element-batched > gpurun_out/${T}_bench.txt 2>&1
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench.txt 2>&1
 timeout 300 python bench.py --impl reference --steps 20 --warmup 2 > gpurun_out/${T}_bench_ref.txt 2>&1
-timeout 300 python bench.py --dtype f32 --no-cpu > gpurun_out/${T}_bench_f32.txt 2>&1
-timeout 600 python bench.py --ne 262144 --inputs device --steps 40 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_c3_f64.txt 2>&1
-timeout 600 python bench.py --ne 262144 --inputs device --dtype f32 --steps 40 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_c4_f32.txt 2>&1
+timeout 300 python bench.py --dtype f32 --no-cpu --no-sweep > gpurun_out/${T}_bench_f32.txt 2>&1
+timeout 600 python bench.py --ne 262144 --inputs device --steps 40 --warmup 3 --no-e2e --no-cpu --no-sweep --no-fp32 > gpurun_out/${T}_c3_f64.txt 2>&1
+timeout 600 python bench.py --ne 262144 --inputs device --dtype f32 --steps 40 --warmup 3 --no-e2e --no-cpu --no-sweep > gpurun_out/${T}_c4_f32.txt 2>&1
 timeout 900 python bench.py --sweep > gpurun_out/${T}_sweep_f64.txt 2>&1
 timeout 900 python bench.py --sweep --dtype f32 > gpurun_out/${T}_sweep_f32.txt 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-emitted > gpurun_out/${T}_ncu_launch.log 2>&1
