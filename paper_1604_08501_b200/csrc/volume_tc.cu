@@ -704,15 +704,21 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
     __syncthreads();  // ft complete; the stage is dead -> S and T-out tiles live in it
 
     // ---- phase 2: per field, written back as soon as T is exchanged ------
+    // (rhsq of field b+1 is loaded while field b computes)
+    auto ld_rh = [&](int b, double &r0, double &r1) {
+      if (PAD) {
+        r0 = vld[0] ? (double)re[qo + b * NPTR] : 0.0;
+        r1 = vld[1] ? (double)re[qo + b * NPTR + 1] : 0.0;
+      } else {
+        ld_pair(re + qo + b * NPTR, r0, r1);
+      }
+    };
+    double rn0, rn1;
+    ld_rh(0, rn0, rn1);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      double rh0, rh1;
-      if (PAD) {
-        rh0 = vld[0] ? (double)re[qo + b * NPTR] : 0.0;
-        rh1 = vld[1] ? (double)re[qo + b * NPTR + 1] : 0.0;
-      } else {
-        ld_pair(re + qo + b * NPTR, rh0, rh1);
-      }
+      const double rh0 = rn0, rh1 = rn1;
+      if (b < 7) ld_rh(b + 1, rn0, rn1);
       double fr[2], fs[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
