@@ -76,7 +76,7 @@ int resolve(int variant, int bytes, int nq) {
     // precisions (round 2, profiles/r02_sweep_*.jsonl)
     if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::col_available(bytes, nq)) {
-      if (nq == 5 || nq == 6) return LFB_VARIANT_COL;
+      if (nq == 5 || (nq == 6 && bytes == 4)) return LFB_VARIANT_COL;
       if (bytes == 4 && nq >= 9 && nq <= 12) return LFB_VARIANT_COL;
       if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }
