@@ -524,6 +524,12 @@ struct TcLeanCfg {
   // element n starts (its stage was element n-1's, free after n-1's last
   // barrier); at Nq = 7 two stages would leave one CTA per SM
   static constexpr int NSTG = (NW < 8 && SUB <= 6) ? 2 : 1;  // Nq=7: 2 stages -> 1 CTA/SM
+  // NW < 8 with one stage (Nq = 7): the S and T-out tiles get their own
+  // space, so the stage is dead right after phase 1 and the next element's
+  // copy is issued then, not after the write-back (0.77 -> 0.82 of HBM; at
+  // Nq 5, 6 own tiles with 1 or 2 stages measured no better than the ring,
+  // profiles/r02_tc_plane.txt)
+  static constexpr bool OWN_TILES = NW < 8 && NSTG == 1;
   static_assert(NW == 8 || PAD, "plane variant is for the zero-padded Nq");
   static_assert(LEAN_STILE + NW * ST_SZ <= STAGE * (int)sizeof(T) / (int)sizeof(double),
                 "aliases fit in the stage");
@@ -532,6 +538,7 @@ struct TcLeanCfg {
 template <typename T, int SUB, int NW>
 struct TcSmemLean {
   T stage[TcLeanCfg<T, SUB, NW>::NSTG][TcLeanCfg<T, SUB, NW>::STAGE];
+  double tiles[TcLeanCfg<T, SUB, NW>::OWN_TILES ? LEAN_STILE + NW * ST_SZ : 2];  // (keeps ft 16-byte aligned)
   double ft[8 * FT_FS];
   unsigned long long bar[TcLeanCfg<T, SUB, NW>::NSTG];
 };
@@ -544,6 +551,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TcSmemLean<T, SUB, NW> &sm = *reinterpret_cast<TcSmemLean<T, SUB, NW> *>(smem_raw);
   constexpr int NSTG = TcLeanCfg<T, SUB, NW>::NSTG;
+  constexpr bool OWN_TILES = TcLeanCfg<T, SUB, NW>::OWN_TILES;
   if (NW < 8) {  // F_t planes k >= SUB have no owner warp: they stay zero
     for (int x = threadIdx.x; x < 8 * FT_FS; x += 32 * NW) sm.ft[x] = 0.0;
   }
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
   for (int64_t n = 0; n < nmine; ++n) {
     const int64_t e = e0 + n * G;
     const int st = (int)(n % NSTG);
-    double *const alias = reinterpret_cast<double *>(sm.stage[st]);
+    double *const alias = OWN_TILES ? sm.tiles : reinterpret_cast<double *>(sm.stage[st]);
     if (NSTG == 2 && tid == 0 && n + 1 < nmine) {
       fence_proxy_async();  // the other stage's last reads were before the previous barrier
       issue(n + 1);
@@ -628,7 +636,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       const int64_t en = e + G;
       const T *sp;
       uint32_t sb_;
-      if (NSTG == 1 && tid == 0) {
+      if (NSTG == 1 && !OWN_TILES && tid == 0) {
         prefetch_l2(q + en * SLABQ, SLABQ * sizeof(T));
         span16(g + en * SLABG, SLABG, sp, sb_);
         prefetch_l2(sp, sb_);
@@ -702,6 +710,10 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       }
     }
     __syncthreads();  // ft complete; the stage is dead -> S and T-out tiles live in it
+    if (OWN_TILES && tid == 0 && n + 1 < nmine) {  // (or have their own space)
+      fence_proxy_async();
+      issue(n + 1);
+    }
 
     // ---- phase 2: per field, written back as soon as T is exchanged ------
     // (rhsq of field b+1 is loaded while field b computes)
@@ -765,7 +777,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       }
     }
     __syncthreads();  // every alias read done: the stage may be refilled
-    if (NSTG == 1 && tid == 0 && n + 1 < nmine) {
+    if (NSTG == 1 && !OWN_TILES && tid == 0 && n + 1 < nmine) {
       fence_proxy_async();
       issue(n + 1);
     }
