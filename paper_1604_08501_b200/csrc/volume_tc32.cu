@@ -142,24 +142,31 @@ constexpr int ST_RS = 8, ST_SZ = 8 * ST_RS;
 // conflicts of the 2 KB slab stride otherwise; see volume_tc.cu)
 constexpr int STAGE_ALLOC = STAGE + 16 * 16;
 
-template <int NS>
+// NW = 8: the virtual Nq=8 cube. NW = SUB < 8 (zero-padded Nq = 5..7, the
+// PLANE variant as in volume_tc.cu): one warp per real k-plane, stages sized
+// for the real q + g slab (+ the g superset's 16-byte shift), F_t planes
+// k >= SUB zeroed once, three CTAs per SM.
+template <int NS, int SUB, int NW>
 struct Smem32 {
-  float stage[NS][STAGE_ALLOC];
+  static constexpr int STAGE_N = NW == 8 ? STAGE_ALLOC : ((17 * SUB * SUB * SUB + 4 + 3) & ~3);
+  float stage[NS][STAGE_N];
   float ft[8 * FT_FS];
   float tout[8 * TO_FS];
-  float stile[WARPS][2][ST_SZ];
+  float stile[NW][2][ST_SZ];
   unsigned long long bar[NS];
 };
 
-// NS = 2: 108 KB of shared memory -> two CTAs (16 warps) per SM; NS = 3:
-// one CTA with a deeper ring
-template <int NS, int SUB>
-__global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
+// NS = 2, NW = 8: 108 KB of shared memory -> two CTAs (16 warps) per SM
+template <int NS, int SUB, int NW = WARPS>
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <= 6 ? 3 : 2))
     volume_tc32_kernel(int64_t ne, float p0, float R, float gam, const float *__restrict__ q,
                        float *__restrict__ rhsq, const float *__restrict__ D,
                        const float *__restrict__ g, const float *__restrict__ jinv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem32<NS> &sm = *reinterpret_cast<Smem32<NS> *>(smem_raw);
+  Smem32<NS, SUB, NW> &sm = *reinterpret_cast<Smem32<NS, SUB, NW> *>(smem_raw);
+  if (NW < 8) {  // F_t planes k >= SUB have no owner warp: they stay zero
+    for (int x = threadIdx.x; x < 8 * FT_FS; x += 32 * NW) sm.ft[x] = 0.f;
+  }
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
@@ -419,8 +426,13 @@ __global__ void __launch_bounds__(THREADS, NS == 2 ? 2 : 1)
 template <int NS, int SUB>
 int launch_tc32(int64_t ngroups, float p0, float R, float gam, const float *q, float *rhsq,
                 const float *D, const float *g, const float *jinv, cudaStream_t stream) {
-  const size_t smem = sizeof(Smem32<NS>);
-  auto kern = volume_tc32_kernel<NS, SUB>;
+  constexpr bool PAD_ = !(SUB == 8 || SUB == 4 || SUB == 2);
+  // PLANE for the zero-padded Nq (8 warps -> SUB warps: Nq 5 / 6 / 7 from
+  // 0.33 / 0.50 / 0.72 to 0.48 / 0.61 / 0.74 of HBM, profiles/r02_tc_plane.txt)
+  constexpr int NW = PAD_ ? SUB : WARPS;
+  const size_t smem = sizeof(Smem32<NS, SUB, NW>);
+  auto kern = volume_tc32_kernel<NS, SUB, NW>;
+  constexpr int THREADS = 32 * NW;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return LFB_ERR_CUDA;
