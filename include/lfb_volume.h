@@ -87,10 +87,12 @@ enum {
     LFB_VARIANT_LINES = 4,   /* Nq 9..13: DMMA line GEMMs over shared flux tiles */
     LFB_VARIANT_COL = 5,     /* Nq 2..12 (fp32: ..16): column owners, FMA in the storage
                                 precision, fluxes through shared line tiles */
-    LFB_VARIANT_LT = 6       /* fp64 Nq 9..12: line tiles — R on the DMMA pipe from the
+    LFB_VARIANT_LT = 6,      /* fp64 Nq 9..12: line tiles — R on the DMMA pipe from the
                                 point owner's registers, S/T through swizzled shared
                                 tiles, per-field q/g stages by bulk copy, software-
                                 pipelined over (element, field) */
+    LFB_VARIANT_LTU = 7      /* fp32 Nq 9..11: the three derivatives as tcgen05 (UMMA)
+                                GEMMs, operands in shared memory, accumulators in TMEM */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -38,8 +38,10 @@ VARIANT_TC = 3
 VARIANT_LINES = 4
 VARIANT_COL = 5
 VARIANT_LT = 6
+VARIANT_LTU = 7
 VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
-            "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL, "lt": VARIANT_LT}
+            "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL, "lt": VARIANT_LT,
+            "ltu": VARIANT_LTU}
 
 MAX_NQ = 16
 

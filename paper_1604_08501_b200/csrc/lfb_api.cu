@@ -34,6 +34,9 @@ int volume_lt_f64(int, int64_t, double, double, double, const double *, double *
 bool lt_available(int dtype_bytes, int nq);
 int volume_lt_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                   const float *, const float *, cudaStream_t);
+int volume_ltu_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                   const float *, const float *, cudaStream_t);
+bool ltu_available(int dtype_bytes, int nq);
 int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
                    const double *, const double *, const double *, cudaStream_t);
 int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
@@ -118,6 +121,8 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
     case LFB_VARIANT_LT:
       if (!lfb::lt_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lt_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LTU:
+      return LFB_ERR_BAD_VARIANT;
     case LFB_VARIANT_COL:
       if (!lfb::col_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -151,6 +156,9 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
     case LFB_VARIANT_LT:
       if (!lfb::lt_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lt_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LTU:
+      if (!lfb::ltu_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_ltu_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_COL:
       if (!lfb::col_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -190,6 +198,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return lfb::col_available(dtype_bytes, Nq) ? 1 : 0;
     case LFB_VARIANT_LT:
       return lfb::lt_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_LTU:
+      return lfb::ltu_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -208,6 +218,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_LINES: return "lines";
     case LFB_VARIANT_COL: return "col";
     case LFB_VARIANT_LT: return "lt";
+    case LFB_VARIANT_LTU: return "ltu";
     default: return "unknown";
   }
 }

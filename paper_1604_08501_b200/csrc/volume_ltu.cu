@@ -1,0 +1,378 @@
+// LFB_VARIANT_LTU, fp32 storage, Nq 9..11 — the three derivatives as
+// tcgen05 (UMMA) GEMMs: operands staged in shared memory, accumulators in
+// TMEM, issued by one thread (SASS: UTCHMMA / UTCBAR / LDTM).
+//
+// Why: the mma.sync line-tile kernel (volume_lt32.cu) is
+// issue-bound at 19-30 warp-instructions per point — fragment loads, tf32
+// splits and HMMAs in every warp, plus the M/K padding of the m16n8k8 tiles
+// at Nq 9..11. Here every direction d in {R, S, T} is ONE M=128 GEMM per
+// field:
+//     C_d^T[line][out] = sum_n X_d^T[line][n] D^T[n][out]
+// with the Nq^2 <= 128 lines of the direction as M (R: (j,k), S: (i,k),
+// T: (i,j)), N = 16 outputs (Nq padded), K = 16 contracted positions (two
+// K=8 steps). fp32 accuracy on TF32 inputs: the owners store each flux split
+// x = x_hi + x_lo (top 19 bits by an ALU mask) into two operand tiles, and
+// the accumulator takes X_hi D_hi + X_lo D_hi + X_hi D_lo (the dropped
+// X_lo D_lo is ~2^-22 relative).
+//
+// Per element (one CTA, persistent grid, two CTAs per SM), per field in the
+// order 1 4 2 5 3 6 0 7 (one g stage serves the momentum fields):
+//   owners (4 points per thread, strided — coalesced global accesses):
+//     fluxes from the q / g stages -> split -> the three K-major operand
+//     tiles (the SWIZZLE_NONE canonical layout: 8-row x 16-byte core
+//     matrices, K-adjacent ones 128 B apart, 8-row groups 512 B apart)
+//   | barrier | thread 0: 18 UMMAs (3 directions x 2 K steps x 3 split
+//   products) -> tcgen05.commit -> mbarrier; warps 0..3 wait, LDTM their
+//   32 TMEM lanes (= lines) x 16 columns (= outputs) and park them in
+//   line-major exchange tiles | barrier | owners: rhsq += Jinv (R + S + T).
+// q_b slabs are bulk-copied two fields ahead, g(b-1, .) one field ahead,
+// the next element's phase-1 inputs L2-prefetched.
+
+#include <stdint.h>
+
+#include "lfb_common.cuh"
+#include "lfb_tma.cuh"
+
+namespace lfb {
+namespace {
+
+__device__ __forceinline__ uint32_t ltu_split_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+
+// byte offset of element (row, k) of a K-major operand tile (K = 16 tf32):
+// core matrices of 8 rows x 16 bytes; LBO = 128 (K-adjacent), SBO = 512
+__device__ __forceinline__ int ltu_off(int row, int k) {
+  return (row >> 3) * 512 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4;
+}
+
+__device__ __forceinline__ uint64_t ltu_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
+}
+
+// field processed at position p (momentum fields on even positions)
+__device__ __forceinline__ int ltu_field(int p) {
+  return (p & 1) ? (p == 7 ? 7 : 4 + (p >> 1)) : (p == 6 ? 0 : 1 + (p >> 1));
+}
+
+template <int NQ>
+struct LtuCfg {
+  static constexpr int NPT = NQ * NQ * NQ;
+  static constexpr int NL = NQ * NQ;                // lines per direction (<= 128)
+  static constexpr int P = 4;                       // points per thread
+  static constexpr int THREADS = ((NPT + P - 1) / P + 31) / 32 * 32;
+  static constexpr int CRS = 17;                    // exchange-tile row stride (odd)
+  static constexpr int SLAB = (NPT + 4 + 3) & ~3;   // stage slab (16-byte aligned superset)
+  static constexpr int AT = 128 * 16;               // one operand tile (floats)
+  // A tiles [dir 3][hi, lo], B tiles [hi, lo] (16 x 16), exchange tiles
+  // [dir 3][128][CRS], q stages [2], g stage [3]
+  static constexpr size_t SMEM = sizeof(float) * (6 * (size_t)AT + 2 * 256 +
+                                                  3 * 128 * (size_t)CRS + 5 * (size_t)SLAB) +
+                                 4 * sizeof(uint64_t) + 16;
+  static_assert(NL <= 128, "one M=128 tile per direction");
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
+    volume_ltu_kernel(int64_t ne, float p0, float R, float gam, const float *__restrict__ q,
+                      float *__restrict__ rhsq, const float *__restrict__ D,
+                      const float *__restrict__ g, const float *__restrict__ jinv) {
+  using C = LtuCfg<NQ>;
+  constexpr int NPT = C::NPT, P = C::P, T = C::THREADS, AT = C::AT, CRS = C::CRS;
+  constexpr int SLAB = C::SLAB, NQQ = NQ * NQ;
+  extern __shared__ __align__(1024) float u_sm[];
+  float *At = u_sm;                 // [dir][hl][AT]
+  float *Bt = At + 6 * AT;          // [hl][256]
+  float *Xc = Bt + 512;             // [dir][128][CRS]
+  float *qst = Xc + 3 * 128 * CRS;  // [2][SLAB]
+  float *gst = qst + 2 * SLAB;      // [3][SLAB]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gst + 3 * SLAB);  // q0, q1, g, mma
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const float Rp0 = R / p0;
+  char *const Ab = reinterpret_cast<char *>(At);
+
+  for (int x = tid; x < 6 * AT + 512; x += T) u_sm[x] = 0.f;
+  __syncthreads();
+  // B = D^T hi / lo: B[row = out][k = n] = D(out, n)
+  for (int x = tid; x < NQ * NQ; x += T) {
+    const int out = x % NQ, n = x / NQ;
+    const float v = __ldg(D + n * NQ + out);
+    const uint32_t hi = ltu_split_hi(v);
+    Bt[ltu_off(out, n) / 4] = __uint_as_float(hi);
+    Bt[256 + ltu_off(out, n) / 4] = v - __uint_as_float(hi);
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) mbar_init(&bars[x], 1);
+    mbar_init_fence();
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  // ---- own points p = tid + m T: offsets in the operand and exchange tiles --
+  int pt[P];
+  bool vp[P];
+  int aR[P], aS[P], aT[P], xR[P], xS[P], xT[P];
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    const int p = tid + m * T;
+    vp[m] = p < NPT;
+    pt[m] = vp[m] ? p : 0;
+    const int i = pt[m] % NQ, j = (pt[m] / NQ) % NQ, k = pt[m] / NQQ;
+    aR[m] = ltu_off(k * NQ + j, i) / 4;  // R line (j,k), K index i
+    aS[m] = ltu_off(k * NQ + i, j) / 4;  // S line (i,k), K index j
+    aT[m] = ltu_off(j * NQ + i, k) / 4;  // T line (i,j), K index k
+    xR[m] = (k * NQ + j) * CRS + i;      // exchange tiles: [line][out]
+    xS[m] = (k * NQ + i) * CRS + j;
+    xT[m] = (j * NQ + i) * CRS + k;
+  }
+
+  // ---- stages (thread 0) ---------------------------------------------------
+  auto slab_bytes = [&](const float *a0) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + NPT) + 15) & ~(uintptr_t)15;
+    return (uint32_t)(hi - lo);
+  };
+  auto slab_copy = [&](float *dst, const float *a0, uint64_t *bar) {
+    bulk_g2s(dst, reinterpret_cast<const void *>(reinterpret_cast<uintptr_t>(a0) & ~(uintptr_t)15),
+             slab_bytes(a0), bar);
+  };
+  auto shift = [](const float *a0) { return (int)((reinterpret_cast<uintptr_t>(a0) & 15) >> 2); };
+  auto issue_q = [&](int64_t e, int p) {
+    const float *a0 = q + (e * 8 + ltu_field(p)) * NPT;
+    mbar_expect_tx(&bars[p & 1], slab_bytes(a0));
+    slab_copy(qst + (p & 1) * SLAB, a0, &bars[p & 1]);
+  };
+  auto issue_g = [&](int64_t e, int b) {
+    uint32_t total = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) total += slab_bytes(g + (e * 9 + 3 * d + b - 1) * NPT);
+    mbar_expect_tx(&bars[2], total);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) slab_copy(gst + d * SLAB, g + (e * 9 + 3 * d + b - 1) * NPT, &bars[2]);
+  };
+  // instruction descriptor: D f32, A / B tf32, both K-major, N = 16, M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) |
+                         ((uint32_t)(128 >> 4) << 24);
+  const uint32_t a_base = smem_u32(At), b_base = smem_u32(Bt);
+  auto umma = [&](uint32_t dcol, uint32_t aaddr, uint32_t baddr, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + dcol),
+        "l"(ltu_desc(aaddr)), "l"(ltu_desc(baddr)), "r"(idesc), "r"(acc));
+  };
+
+  int64_t e = blockIdx.x;
+  if (tid == 0 && e < ne) {
+    issue_q(e, 0);
+    issue_q(e, 1);
+    issue_g(e, ltu_field(0));
+  }
+  uint32_t gpar = 0, mpar = 0;
+  float rhn[P];
+  if (e < ne) {
+#pragma unroll
+    for (int m = 0; m < P; ++m) rhn[m] = vp[m] ? rhsq[(e * 8 + ltu_field(0)) * NPT + pt[m]] : 0.f;
+  }
+  for (; e < ne; e += gridDim.x) {
+    const float *qe = q + e * 8 * NPT;
+    const float *ge = g + e * 9 * NPT;
+    float *re = rhsq + e * 8 * NPT;
+    const int64_t en = e + gridDim.x;
+
+    // ---- phase 1: W_d = V_d / rho, p, Jinv (FP32) ---------------------------
+    float Wd[3][P], pp[P], jv[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      const int o = pt[m];
+      const bool v = vp[m];
+      const float rr = v ? __ldg(qe + o) : 1.f, th = v ? __ldg(qe + 4 * NPT + o) : 1.f;
+      float U[3], gv[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) U[a] = v ? __ldg(qe + (1 + a) * NPT + o) : 0.f;
+#pragma unroll
+      for (int x = 0; x < 9; ++x) gv[x] = v ? __ldg(ge + x * NPT + o) : 0.f;
+      jv[m] = v ? __ldg(jinv + e * NPT + o) : 0.f;
+      const float rinv = __frcp_rn(rr);
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        Wd[d][m] = fmaf(gv[3 * d], U[0], fmaf(gv[3 * d + 1], U[1], gv[3 * d + 2] * U[2])) * rinv;
+      pp[m] = p0 * exp2f(gam * log2f(Rp0 * th));
+    }
+
+#pragma unroll 1
+    for (int p = 0; p < 8; ++p) {
+      const int b = ltu_field(p);
+      const bool mom = b >= 1 && b <= 3;
+      float part[P];
+      {
+        const int bn = ltu_field((p + 1) & 7);
+        const float *rnext = p < 7 ? re + bn * NPT : rhsq + (en * 8 + bn) * NPT;
+        const bool have = p < 7 || en < ne;
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          part[m] = rhn[m];
+          rhn[m] = (have && vp[m]) ? rnext[pt[m]] : 0.f;
+        }
+      }
+      mbar_wait(&bars[p & 1], (uint32_t)((p >> 1) & 1));
+      if (mom) {
+        mbar_wait(&bars[2], gpar);
+        gpar ^= 1u;
+      }
+      // ---- fluxes -> split operand tiles -------------------------------------
+      {
+        const float *qs = qst + (p & 1) * SLAB + shift(q + (e * 8 + b) * NPT);
+        const float *gs0 = gst + shift(g + (e * 9 + b - 1) * NPT);
+        const float *gs1 = gst + SLAB + shift(g + (e * 9 + 3 + b - 1) * NPT);
+        const float *gs2 = gst + 2 * SLAB + shift(g + (e * 9 + 6 + b - 1) * NPT);
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          if (!vp[m]) continue;
+          const float qv = qs[pt[m]];
+          float f[3] = {Wd[0][m] * qv, Wd[1][m] * qv, Wd[2][m] * qv};
+          if (mom) {
+            f[0] = fmaf(gs0[pt[m]], pp[m], f[0]);
+            f[1] = fmaf(gs1[pt[m]], pp[m], f[1]);
+            f[2] = fmaf(gs2[pt[m]], pp[m], f[2]);
+          }
+          const int off[3] = {aR[m], aS[m], aT[m]};
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const uint32_t hi = ltu_split_hi(f[d]);
+            At[(2 * d) * AT + off[d]] = __uint_as_float(hi);
+            At[(2 * d + 1) * AT + off[d]] = f[d] - __uint_as_float(hi);
+          }
+        }
+      }
+      if (p == 6 && tid == 32 && en < ne) {  // next element's phase-1 inputs into L2
+        prefetch_l2_range(q + en * 8 * NPT, 5ull * NPT * sizeof(float));
+        prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(float));
+        prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(float));
+      }
+      fence_proxy_async();  // operand stores -> visible to the tensor core
+      __syncthreads();      // operands complete; stage reads of position p done
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const uint32_t ah = a_base + (2 * d) * AT * 4, al = ah + AT * 4;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            umma(16 * d, ah + ks * 256, b_base + ks * 256, ks > 0);
+            umma(16 * d, al + ks * 256, b_base + ks * 256, 1);
+            umma(16 * d, ah + ks * 256, b_base + 1024 + ks * 256, 1);
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&bars[3])));
+        fence_proxy_async();
+        if (p + 2 < 8) issue_q(e, p + 2);
+        else if (en < ne) issue_q(en, p - 6);
+        if (p == 0 || p == 2) issue_g(e, ltu_field(p + 2));
+        else if (p == 4 && en < ne) issue_g(en, ltu_field(0));
+      }
+      // ---- TMEM -> exchange tiles (warps 0..3: lanes = lines) ------------------
+      if (w < 4) {
+        mbar_wait(&bars[3], mpar);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int line = 32 * w + lane;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+              "%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tmem + ((uint32_t)(32 * w) << 16) + 16 * d));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (line < C::NL) {
+#pragma unroll
+            for (int o = 0; o < NQ; ++o) Xc[(d * 128 + line) * CRS + o] = __uint_as_float(v[o]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+      }
+      mpar ^= 1u;
+      __syncthreads();  // exchange tiles complete; the MMAs have read the operands
+      // ---- rhsq_b += Jinv (R + S + T) ----------------------------------------------
+#pragma unroll
+      for (int m = 0; m < P; ++m)
+        if (vp[m])
+          re[b * NPT + pt[m]] =
+              fmaf(jv[m], Xc[xR[m]] + Xc[128 * CRS + xS[m]] + Xc[256 * CRS + xT[m]], part[m]);
+    }
+  }
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+}
+
+template <int NQ>
+int launch_ltu(int64_t ne, float p0, float R, float gam, const float *q, float *rhsq,
+               const float *D, const float *g, const float *jinv, cudaStream_t s) {
+  using C = LtuCfg<NQ>;
+  auto kern = volume_ltu_kernel<NQ>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return LFB_ERR_CUDA;
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM) !=
+          cudaSuccess)
+    return LFB_ERR_CUDA;
+  if (per_sm < 1) return LFB_ERR_LAUNCH;
+  if (per_sm > 2) per_sm = 2;  // 64 TMEM columns per CTA; keep allocations uncontended
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t grid = ne < slots ? ne : slots;
+  if (grid == 0) return LFB_OK;
+  kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(ne, p0, R, gam, q, rhsq, D, g, jinv);
+  LFB_CHECK_LAUNCH();
+  return LFB_OK;
+}
+
+int dispatch_ltu(int nq, int64_t ne, float p0, float R, float gam, const float *q, float *rhsq,
+                 const float *D, const float *g, const float *jinv, cudaStream_t s) {
+  switch (nq) {
+    case 9: return launch_ltu<9>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 10: return launch_ltu<10>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    case 11: return launch_ltu<11>(ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+    default: return LFB_ERR_BAD_VARIANT;
+  }
+}
+
+}  // namespace
+
+bool ltu_available(int dtype_bytes, int nq) { return dtype_bytes == 4 && nq >= 9 && nq <= 11; }
+int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                   const float *, const float *, cudaStream_t);
+
+// 16-byte aligned q / g needed by the bulk copies (else: the column kernel);
+// for odd Nq the last element goes to the column kernel (its slab superset
+// would leave the arrays)
+int volume_ltu_f32(int nq, int64_t ne, float p0, float R, float gam, const float *q, float *rhsq,
+                   const float *D, const float *g, const float *jinv, cudaStream_t s) {
+  if (!ltu_available(4, nq)) return LFB_ERR_BAD_VARIANT;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(g)) & 15)
+    return volume_col_f32(nq, ne, p0, R, gam, q, rhsq, D, g, jinv, s);
+  const int64_t npt = (int64_t)nq * nq * nq;
+  const int64_t n = ((npt * 4) % 16 && ne > 0) ? ne - 1 : ne;
+  int rc = n > 0 ? dispatch_ltu(nq, n, p0, R, gam, q, rhsq, D, g, jinv, s) : LFB_OK;
+  if (rc != LFB_OK || n == ne) return rc;
+  return volume_col_f32(nq, ne - n, p0, R, gam, q + n * 8 * npt, rhsq + n * 8 * npt, D,
+                        g + n * 9 * npt, jinv + n * npt, s);
+}
+
+}  // namespace lfb

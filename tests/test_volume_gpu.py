@@ -29,7 +29,7 @@ SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (2, 130, 3), (3, 2, 3), (3, 33, 4), (
 
 
 def _variants(nbytes, nq):
-    return [v for v in ("basic", "fused", "tc", "lines", "col", "lt")
+    return [v for v in ("basic", "fused", "tc", "lines", "col", "lt", "ltu")
             if _native.variant_available(v, nbytes, nq)]
 
 
