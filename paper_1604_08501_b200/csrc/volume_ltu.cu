@@ -44,6 +44,33 @@ __device__ __forceinline__ int ltu_off(int row, int k) {
   return (row >> 3) * 512 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4;
 }
 
+__device__ __forceinline__ bool ltu_elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void ltu_ld16(uint32_t (&v)[16], uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];\n tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void ltu_ld8(uint32_t (&v)[8], uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+      " tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ uint64_t ltu_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
@@ -58,7 +85,7 @@ template <int NQ>
 struct LtuCfg {
   static constexpr int NPT = NQ * NQ * NQ;
   static constexpr int NL = NQ * NQ;                // lines per direction (<= 128)
-  static constexpr int P = 4;                       // points per thread
+  static constexpr int P = NQ == 9 ? 3 : NQ == 10 ? 4 : 5;  // points per thread (>= 8 warps)
   static constexpr int THREADS = ((NPT + P - 1) / P + 31) / 32 * 32;
   static constexpr int CRS = 17;                    // exchange-tile row stride (odd)
   static constexpr int SLAB = (NPT + 4 + 3) & ~3;   // stage slab (16-byte aligned superset)
@@ -67,8 +94,9 @@ struct LtuCfg {
   // [dir 3][128][CRS], q stages [2], g stage [3]
   static constexpr size_t SMEM = sizeof(float) * (6 * (size_t)AT + 2 * 256 +
                                                   3 * 128 * (size_t)CRS + 5 * (size_t)SLAB) +
-                                 4 * sizeof(uint64_t) + 16;
+                                 6 * sizeof(uint64_t) + 16;
   static_assert(NL <= 128, "one M=128 tile per direction");
+  static_assert(THREADS >= 256, "eight TMEM reader warps");
 };
 
 template <int NQ>
@@ -85,8 +113,8 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   float *Xc = Bt + 512;             // [dir][128][CRS]
   float *qst = Xc + 3 * 128 * CRS;  // [2][SLAB]
   float *gst = qst + 2 * SLAB;      // [3][SLAB]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gst + 3 * SLAB);  // q0, q1, g, mma
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gst + 3 * SLAB);  // q0, q1, g, mma R, S, T
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const float Rp0 = R / p0;
@@ -110,7 +138,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   }
   if (tid == 0) {
 #pragma unroll
-    for (int x = 0; x < 4; ++x) mbar_init(&bars[x], 1);
+    for (int x = 0; x < 6; ++x) mbar_init(&bars[x], 1);
     mbar_init_fence();
   }
   fence_proxy_async();
@@ -262,45 +290,58 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
       }
       fence_proxy_async();  // operand stores -> visible to the tensor core
       __syncthreads();      // operands complete; stage reads of position p done
-      if (tid == 0) {
+      if (w == 0) {  // one elected lane issues; each direction commits to its own barrier
         asm volatile("tcgen05.fence::after_thread_sync;");
+        if (ltu_elect_one()) {
+          const int dord[3] = {0, 1, 2};
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const uint32_t ah = a_base + (2 * d) * AT * 4, al = ah + AT * 4;
+          for (int x = 0; x < 3; ++x) {
+            const int d = dord[x];
+            const uint32_t ah = a_base + (2 * d) * AT * 4, al = ah + AT * 4;
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            umma(16 * d, ah + ks * 256, b_base + ks * 256, ks > 0);
-            umma(16 * d, al + ks * 256, b_base + ks * 256, 1);
-            umma(16 * d, ah + ks * 256, b_base + 1024 + ks * 256, 1);
+            for (int ks = 0; ks < 2; ++ks) {
+              umma(16 * d, ah + ks * 256, b_base + ks * 256, ks > 0);
+              umma(16 * d, al + ks * 256, b_base + ks * 256, 1);
+              umma(16 * d, ah + ks * 256, b_base + 1024 + ks * 256, 1);
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    smem_u32(&bars[3 + d])));
           }
+          fence_proxy_async();
+          if (p + 2 < 8) issue_q(e, p + 2);
+          else if (en < ne) issue_q(en, p - 6);
+          if (p == 0 || p == 2) issue_g(e, ltu_field(p + 2));
+          else if (p == 4 && en < ne) issue_g(en, ltu_field(0));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&bars[3])));
-        fence_proxy_async();
-        if (p + 2 < 8) issue_q(e, p + 2);
-        else if (en < ne) issue_q(en, p - 6);
-        if (p == 0 || p == 2) issue_g(e, ltu_field(p + 2));
-        else if (p == 4 && en < ne) issue_g(en, ltu_field(0));
+        __syncwarp();
       }
-      // ---- TMEM -> exchange tiles (warps 0..3: lanes = lines) ------------------
-      if (w < 4) {
-        mbar_wait(&bars[3], mpar);
+      // ---- TMEM -> exchange tiles: warps 0..3 take R and T outputs 0..7, warps
+      // 4..7 S and T outputs 8..15 (a warp reads the 32 lanes of quadrant w % 4)
+      if (w < 8) {
+        const int line = 32 * (w & 3) + lane;
+        const uint32_t tq = tmem + ((uint32_t)(32 * (w & 3)) << 16);
+        const int d0 = w < 4 ? 0 : 1;
+        mbar_wait(&bars[3 + d0], mpar);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const int line = 32 * w + lane;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
+        {
           uint32_t v[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-              "%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(tmem + ((uint32_t)(32 * w) << 16) + 16 * d));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          ltu_ld16(v, tq + 16 * d0);
           if (line < C::NL) {
 #pragma unroll
-            for (int o = 0; o < NQ; ++o) Xc[(d * 128 + line) * CRS + o] = __uint_as_float(v[o]);
+            for (int o = 0; o < NQ; ++o) Xc[(d0 * 128 + line) * CRS + o] = __uint_as_float(v[o]);
+          }
+        }
+        mbar_wait(&bars[5], mpar);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        {
+          const int o0 = w < 4 ? 0 : 8;
+          uint32_t v[8];
+          ltu_ld8(v, tq + 32 + o0);
+          if (line < C::NL) {
+#pragma unroll
+            for (int o = 0; o < 8; ++o)
+              if (o0 + o < NQ) Xc[(256 + line) * CRS + o0 + o] = __uint_as_float(v[o]);
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -325,16 +366,24 @@ int launch_ltu(int64_t ne, float p0, float R, float gam, const float *q, float *
   using C = LtuCfg<NQ>;
   auto kern = volume_ltu_kernel<NQ>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
-      cudaSuccess)
+          cudaSuccess ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
     return LFB_ERR_CUDA;
-  int dev = 0, sms = 0, per_sm = 0;
+  // residency from the shared-memory budget: the occupancy API reports one
+  // CTA per SM for this kernel although two fit (the launch bounds guarantee
+  // the registers for two)
+  int dev = 0, sms = 0, smem_sm = 0, reserved = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM) !=
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) !=
+          cudaSuccess ||
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) !=
           cudaSuccess)
     return LFB_ERR_CUDA;
+  int per_sm = smem_sm / ((int)C::SMEM + reserved);
   if (per_sm < 1) return LFB_ERR_LAUNCH;
-  if (per_sm > 2) per_sm = 2;  // 64 TMEM columns per CTA; keep allocations uncontended
+  if (per_sm > 2) per_sm = 2;  // 64 TMEM columns per CTA; the launch bounds cover two
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;

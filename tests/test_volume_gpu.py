@@ -308,3 +308,21 @@ def test_tc16_fp32_many_elements_against_c_oracle(cuda_device, nq, ne):
     want = coracle.volume_f64_eb(nq, q, g, j, d, st.constants)
     err = max_rel_error(coracle.from_element_batched(got), coracle.from_element_batched(want))
     assert err <= TOL32, err
+
+
+@pytest.mark.parametrize("nq,ne", [(9, 701), (10, 650), (11, 613), (12, 597)])
+def test_line_tile_kernels_many_elements_against_c_oracle(cuda_device, nq, ne):
+    """The line-tile kernels (lt fp64 / fp32, ltu fp32 on tcgen05) over more
+    elements than resident CTAs, so every CTA runs several persistent
+    iterations and the stage pipelines wrap across elements; odd Ne puts the
+    last element of odd Nq through the column kernel."""
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=nq + 11))
+    q, g, j, d = coracle.to_element_batched(st)
+    want = coracle.from_element_batched(coracle.volume_f64_eb(nq, q, g, j, d, st.constants))
+    for dtype, nbytes, tol in ((torch.float64, 8, TOL64), (torch.float32, 4, TOL32)):
+        for v in [x for x in ("lt", "ltu") if _native.variant_available(x, nbytes, nq)]:
+            ds = DeviceFieldState.from_field_state(st, dtype=dtype)
+            volume_rhs_device(ds, variant=v)
+            got = ds.rhsq.to(torch.float64).cpu().numpy()
+            err = max_rel_error(coracle.from_element_batched(got), want)
+            assert err <= tol, (v, dtype, err)
