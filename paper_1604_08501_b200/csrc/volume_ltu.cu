@@ -32,16 +32,24 @@
 
 #include "lfb_common.cuh"
 #include "lfb_tma.cuh"
+#ifdef LTU_TIMING
+#include <stdio.h>
+#define LTU_T(k) do { tt[k] = clock64(); } while (0)
+#else
+#define LTU_T(k) do { } while (0)
+#endif
 
 namespace lfb {
 namespace {
 
 __device__ __forceinline__ uint32_t ltu_split_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
 
-// byte offset of element (row, k) of a K-major operand tile (K = 16 tf32):
-// core matrices of 8 rows x 16 bytes; LBO = 128 (K-adjacent), SBO = 512
+// byte offset of element (row, k) of a K-major operand tile (K = 24 tf32):
+// core matrices of 8 rows x 16 bytes; LBO = 128 (K-adjacent), SBO = 768
+constexpr int LTU_K = 24;
+constexpr int LTU_SBO = LTU_K / 4 * 128;
 __device__ __forceinline__ int ltu_off(int row, int k) {
-  return (row >> 3) * 512 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4;
+  return (row >> 3) * LTU_SBO + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4;
 }
 
 __device__ __forceinline__ bool ltu_elect_one() {
@@ -73,7 +81,7 @@ __device__ __forceinline__ void ltu_ld8(uint32_t (&v)[8], uint32_t taddr) {
 
 __device__ __forceinline__ uint64_t ltu_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) |
-         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
+         ((uint64_t)(LTU_SBO >> 4) << 32) | ((uint64_t)1 << 46);  // version 1, SWIZZLE_NONE
 }
 
 // field processed at position p (momentum fields on even positions)
@@ -89,10 +97,11 @@ struct LtuCfg {
   static constexpr int THREADS = ((NPT + P - 1) / P + 31) / 32 * 32;
   static constexpr int CRS = 17;                    // exchange-tile row stride (odd)
   static constexpr int SLAB = (NPT + 4 + 3) & ~3;   // stage slab (16-byte aligned superset)
-  static constexpr int AT = 128 * 16;               // one operand tile (floats)
+  static constexpr int AT = 128 * LTU_K;            // one operand tile (floats)
+  static constexpr int BT = 32 * LTU_K;             // the B tile
   // A tiles [dir 3][hi, lo], B tiles [hi, lo] (16 x 16), exchange tiles
   // [dir 3][128][CRS], q stages [2], g stage [3]
-  static constexpr size_t SMEM = sizeof(float) * (6 * (size_t)AT + 2 * 256 +
+  static constexpr size_t SMEM = sizeof(float) * (3 * (size_t)AT + BT +
                                                   3 * 128 * (size_t)CRS + 5 * (size_t)SLAB) +
                                  6 * sizeof(uint64_t) + 16;
   static_assert(NL <= 128, "one M=128 tile per direction");
@@ -108,9 +117,9 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   constexpr int NPT = C::NPT, P = C::P, T = C::THREADS, AT = C::AT, CRS = C::CRS;
   constexpr int SLAB = C::SLAB, NQQ = NQ * NQ;
   extern __shared__ __align__(1024) float u_sm[];
-  float *At = u_sm;                 // [dir][hl][AT]
-  float *Bt = At + 6 * AT;          // [hl][256]
-  float *Xc = Bt + 512;             // [dir][128][CRS]
+  float *At = u_sm;                 // [dir][AT]
+  float *Bt = At + 3 * AT;          // [BT]
+  float *Xc = Bt + C::BT;           // [dir][128][CRS]
   float *qst = Xc + 3 * 128 * CRS;  // [2][SLAB]
   float *gst = qst + 2 * SLAB;      // [3][SLAB]
   uint64_t *bars = reinterpret_cast<uint64_t *>(gst + 3 * SLAB);  // q0, q1, g, mma R, S, T
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   const float Rp0 = R / p0;
   char *const Ab = reinterpret_cast<char *>(At);
 
-  for (int x = tid; x < 6 * AT + 512; x += T) u_sm[x] = 0.f;
+  for (int x = tid; x < 3 * AT + C::BT; x += T) u_sm[x] = 0.f;
   __syncthreads();
   // B = D^T hi / lo: B[row = out][k = n] = D(out, n)
   for (int x = tid; x < NQ * NQ; x += T) {
@@ -128,12 +137,13 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
     const float v = __ldg(D + n * NQ + out);
     const uint32_t hi = ltu_split_hi(v);
     Bt[ltu_off(out, n) / 4] = __uint_as_float(hi);
-    Bt[256 + ltu_off(out, n) / 4] = v - __uint_as_float(hi);
+    Bt[ltu_off(out, 12 + n) / 4] = __uint_as_float(hi);
+    Bt[ltu_off(16 + out, n) / 4] = v - __uint_as_float(hi);
   }
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(64));
+                 "r"(128));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
     for (int d = 0; d < 3; ++d) slab_copy(gst + d * SLAB, g + (e * 9 + 3 * d + b - 1) * NPT, &bars[2]);
   };
   // instruction descriptor: D f32, A / B tf32, both K-major, N = 16, M = 128
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) |
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
                          ((uint32_t)(128 >> 4) << 24);
   const uint32_t a_base = smem_u32(At), b_base = smem_u32(Bt);
   auto umma = [&](uint32_t dcol, uint32_t aaddr, uint32_t baddr, uint32_t acc) {
@@ -201,6 +211,10 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   };
 
   int64_t e = blockIdx.x;
+#ifdef LTU_TIMING
+  long long acc[10] = {0};
+  const long long tstart = clock64();
+#endif
   if (tid == 0 && e < ne) {
     issue_q(e, 0);
     issue_q(e, 1);
@@ -240,6 +254,11 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
 
 #pragma unroll 1
     for (int p = 0; p < 8; ++p) {
+#ifdef LTU_TIMING
+      long long tt[9] = {0};
+      tt[3] = tt[4] = tt[5] = 0;
+#endif
+      LTU_T(0);
       const int b = ltu_field(p);
       const bool mom = b >= 1 && b <= 3;
       float part[P];
@@ -258,6 +277,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
         mbar_wait(&bars[2], gpar);
         gpar ^= 1u;
       }
+      LTU_T(1);
       // ---- fluxes -> split operand tiles -------------------------------------
       {
         const float *qs = qst + (p & 1) * SLAB + shift(q + (e * 8 + b) * NPT);
@@ -278,8 +298,8 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
             const uint32_t hi = ltu_split_hi(f[d]);
-            At[(2 * d) * AT + off[d]] = __uint_as_float(hi);
-            At[(2 * d + 1) * AT + off[d]] = f[d] - __uint_as_float(hi);
+            At[d * AT + off[d]] = __uint_as_float(hi);
+            At[d * AT + off[d] + 96] = f[d] - __uint_as_float(hi);  // K index 12 + n
           }
         }
       }
@@ -288,8 +308,10 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
         prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(float));
         prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(float));
       }
+      LTU_T(8);
       fence_proxy_async();  // operand stores -> visible to the tensor core
       __syncthreads();      // operands complete; stage reads of position p done
+      LTU_T(2);
       if (w == 0) {  // one elected lane issues; each direction commits to its own barrier
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (ltu_elect_one()) {
@@ -297,13 +319,9 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
 #pragma unroll
           for (int x = 0; x < 3; ++x) {
             const int d = dord[x];
-            const uint32_t ah = a_base + (2 * d) * AT * 4, al = ah + AT * 4;
+            const uint32_t ad = a_base + d * AT * 4;
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              umma(16 * d, ah + ks * 256, b_base + ks * 256, ks > 0);
-              umma(16 * d, al + ks * 256, b_base + ks * 256, 1);
-              umma(16 * d, ah + ks * 256, b_base + 1024 + ks * 256, 1);
-            }
+            for (int ks = 0; ks < LTU_K / 8; ++ks) umma(32 * d, ad + ks * 256, b_base + ks * 256, ks > 0);
             asm volatile(
                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     smem_u32(&bars[3 + d])));
@@ -315,6 +333,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
           else if (p == 4 && en < ne) issue_g(en, ltu_field(0));
         }
         __syncwarp();
+        LTU_T(3);
       }
       // ---- TMEM -> exchange tiles: warps 0..3 take R and T outputs 0..7, warps
       // 4..7 S and T outputs 8..15 (a warp reads the 32 lanes of quadrant w % 4)
@@ -323,41 +342,63 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
         const uint32_t tq = tmem + ((uint32_t)(32 * (w & 3)) << 16);
         const int d0 = w < 4 ? 0 : 1;
         mbar_wait(&bars[3 + d0], mpar);
+        LTU_T(4);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        {
-          uint32_t v[16];
-          ltu_ld16(v, tq + 16 * d0);
+        {  // columns o (X_hi D_hi + X_lo D_hi) and 16 + o (X_hi D_lo)
+          uint32_t v[16], u[16];
+          ltu_ld16(v, tq + 32 * d0);
+          ltu_ld16(u, tq + 32 * d0 + 16);
           if (line < C::NL) {
 #pragma unroll
-            for (int o = 0; o < NQ; ++o) Xc[(d0 * 128 + line) * CRS + o] = __uint_as_float(v[o]);
+            for (int o = 0; o < NQ; ++o)
+              Xc[(d0 * 128 + line) * CRS + o] = __uint_as_float(v[o]) + __uint_as_float(u[o]);
           }
         }
         mbar_wait(&bars[5], mpar);
+        LTU_T(5);
         asm volatile("tcgen05.fence::after_thread_sync;");
         {
           const int o0 = w < 4 ? 0 : 8;
-          uint32_t v[8];
-          ltu_ld8(v, tq + 32 + o0);
+          uint32_t v[8], u[8];
+          ltu_ld8(v, tq + 64 + o0);
+          ltu_ld8(u, tq + 80 + o0);
           if (line < C::NL) {
 #pragma unroll
             for (int o = 0; o < 8; ++o)
-              if (o0 + o < NQ) Xc[(256 + line) * CRS + o0 + o] = __uint_as_float(v[o]);
+              if (o0 + o < NQ)
+                Xc[(256 + line) * CRS + o0 + o] = __uint_as_float(v[o]) + __uint_as_float(u[o]);
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
       }
       mpar ^= 1u;
       __syncthreads();  // exchange tiles complete; the MMAs have read the operands
+      LTU_T(6);
       // ---- rhsq_b += Jinv (R + S + T) ----------------------------------------------
 #pragma unroll
       for (int m = 0; m < P; ++m)
         if (vp[m])
           re[b * NPT + pt[m]] =
               fmaf(jv[m], Xc[xR[m]] + Xc[128 * CRS + xS[m]] + Xc[256 * CRS + xT[m]], part[m]);
+#ifdef LTU_TIMING
+      LTU_T(7);
+      if (tid == 0 || tid == 128) {
+        acc[0] += tt[1] - tt[0]; acc[1] += tt[2] - tt[1];
+        if (tid == 0) acc[2] += tt[3] - tt[2];
+        acc[3] += tt[4] - tt[2]; acc[4] += tt[5] - tt[2]; acc[5] += tt[6] - tt[2];
+        acc[6] += tt[7] - tt[6]; acc[7] += 1; acc[8] += tt[8] - tt[1];
+      }
+#endif
     }
   }
+#ifdef LTU_TIMING
+  if (blockIdx.x < 2 && (tid == 0 || tid == 128))
+    printf("LTUT cta %d tid %d fields %lld total %lld per field: flux %lld q %lld bar1 %lld mma %lld r %lld t %lld bar2 %lld comb %lld\n",
+           blockIdx.x, tid, acc[7], clock64() - tstart, acc[8] / acc[7], acc[0] / acc[7], acc[1] / acc[7], acc[2] / acc[7],
+           acc[3] / acc[7], acc[4] / acc[7], acc[5] / acc[7], acc[6] / acc[7]);
+#endif
   __syncthreads();
-  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
 }
 
 template <int NQ>
@@ -383,7 +424,7 @@ int launch_ltu(int64_t ne, float p0, float R, float gam, const float *q, float *
     return LFB_ERR_CUDA;
   int per_sm = smem_sm / ((int)C::SMEM + reserved);
   if (per_sm < 1) return LFB_ERR_LAUNCH;
-  if (per_sm > 2) per_sm = 2;  // 64 TMEM columns per CTA; the launch bounds cover two
+  if (per_sm > 2) per_sm = 2;  // 128 TMEM columns per CTA; the launch bounds cover two
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t grid = ne < slots ? ne : slots;
   if (grid == 0) return LFB_OK;
