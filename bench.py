@@ -66,6 +66,7 @@ KERNEL_SOURCES = {
     "lines": ("volume_lines.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "lt": ("volume_lt.cu", "lfb_common.cuh", "lfb_math.cuh", "lfb_tma.cuh"),
     "lt32": ("volume_lt32.cu", "lfb_common.cuh", "lfb_tma.cuh"),
+    "ltu": ("volume_ltu.cu", "lfb_common.cuh", "lfb_tma.cuh"),
     "fused": ("volume_fused.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "basic": ("volume_basic.cu", "lfb_common.cuh"),
 }

@@ -76,7 +76,9 @@ int resolve(int variant, int bytes, int nq) {
     // Nq 2, 4, 7, 8 and fp32 Nq 13..16 (the 16x16-plane TF32 kernel); lines
     // keeps fp64 Nq 9..13 (profiles/r01_col_configs.txt, r01_tc16.txt)
     // line tiles (volume_lt*.cu) where they lead: Nq 11, 12 in both
-    // precisions (round 2, profiles/r02_sweep_*.jsonl)
+    // precisions, except fp32 Nq 11 where the tcgen05 line GEMMs
+    // (volume_ltu.cu) lead (round 2, profiles/r02_sweep_*.jsonl)
+    if (nq == 11 && lfb::ltu_available(bytes, nq)) return LFB_VARIANT_LTU;
     if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::col_available(bytes, nq)) {
       if (nq == 5 || (nq == 6 && bytes == 4)) return LFB_VARIANT_COL;

@@ -1,32 +1,43 @@
 // LFB_VARIANT_LTU, fp32 storage, Nq 9..11 — the three derivatives as
 // tcgen05 (UMMA) GEMMs: operands staged in shared memory, accumulators in
-// TMEM, issued by one thread (SASS: UTCHMMA / UTCBAR / LDTM).
+// TMEM, issued by one elected thread (SASS: UTCHMMA / UTCBAR / LDTM).
 //
 // Why: the mma.sync line-tile kernel (volume_lt32.cu) is
 // issue-bound at 19-30 warp-instructions per point — fragment loads, tf32
-// splits and HMMAs in every warp, plus the M/K padding of the m16n8k8 tiles
-// at Nq 9..11. Here every direction d in {R, S, T} is ONE M=128 GEMM per
-// field:
-//     C_d^T[line][out] = sum_n X_d^T[line][n] D^T[n][out]
+// splits and HMMAs in every warp. Here every direction d in {R, S, T} is ONE
+// M=128 GEMM chain per field:
+//     C_d[line][out] = sum_K A_d[line][K] B[out][K]
 // with the Nq^2 <= 128 lines of the direction as M (R: (j,k), S: (i,k),
-// T: (i,j)), N = 16 outputs (Nq padded), K = 16 contracted positions (two
-// K=8 steps). fp32 accuracy on TF32 inputs: the owners store each flux split
-// x = x_hi + x_lo (top 19 bits by an ALU mask) into two operand tiles, and
-// the accumulator takes X_hi D_hi + X_lo D_hi + X_hi D_lo (the dropped
-// X_lo D_lo is ~2^-22 relative).
+// T: (i,j)). fp32 accuracy on TF32 inputs: the owners split each flux
+// x = x_hi + x_lo (top 19 bits by an ALU mask) and store both halves into ONE
+// K-major operand row, x_hi at K = n and x_lo at K = 12 + n (K = 24, three
+// K=8 steps). B is [D_hi | D_hi] in rows 0..15 and [D_lo | 0] in rows 16..31
+// (N = 32), so columns o and 16 + o of the accumulator hold
+// X_hi D_hi + X_lo D_hi and X_hi D_lo (the dropped X_lo D_lo is ~2^-22
+// relative); the readers add them. A K=8 tf32 UMMA costs ~52 cycles for any
+// N <= 64 (tools/scratch-measured), so folding the split into K and N halves
+// the tensor time of the 18-UMMA hi/lo/hi formulation.
 //
 // Per element (one CTA, persistent grid, two CTAs per SM), per field in the
 // order 1 4 2 5 3 6 0 7 (one g stage serves the momentum fields):
-//   owners (4 points per thread, strided — coalesced global accesses):
-//     fluxes from the q / g stages -> split -> the three K-major operand
-//     tiles (the SWIZZLE_NONE canonical layout: 8-row x 16-byte core
-//     matrices, K-adjacent ones 128 B apart, 8-row groups 512 B apart)
-//   | barrier | thread 0: 18 UMMAs (3 directions x 2 K steps x 3 split
-//   products) -> tcgen05.commit -> mbarrier; warps 0..3 wait, LDTM their
-//   32 TMEM lanes (= lines) x 16 columns (= outputs) and park them in
-//   line-major exchange tiles | barrier | owners: rhsq += Jinv (R + S + T).
+//   owners (P points per thread, strided — coalesced global accesses):
+//     fluxes from the q / g stages -> split -> the three operand tiles (the
+//     SWIZZLE_NONE canonical layout: 8-row x 16-byte core matrices,
+//     K-adjacent ones 128 B apart, 8-row groups 768 B apart)
+//   | barrier | warp 0, one elected lane: 9 UMMAs, a tcgen05.commit per
+//   direction to its own mbarrier, then the next stage copies; warps 0..3
+//   read R and T outputs 0..7, warps 4..7 S and T outputs 8..15 (a warp sees
+//   the 32 TMEM lanes of quadrant w % 4) into line-major exchange tiles
+//   | barrier | owners: rhsq += Jinv (R + S + T).
 // q_b slabs are bulk-copied two fields ahead, g(b-1, .) one field ahead,
 // the next element's phase-1 inputs L2-prefetched.
+//
+// Measured (profiles/r02_sweep_f32.jsonl): it leads the mma.sync line tiles
+// at every Nq it covers and is the AUTO kernel at fp32 Nq 11; the column
+// kernel keeps Nq 9, 10. A per-phase clock64 breakdown (-DLTU_TIMING) shows
+// the field cost split between the flux stores (shared-memory bound: the
+// K-major rows give each line only four banks), the UMMA chain and the
+// TMEM readback.
 
 #include <stdint.h>
 
