@@ -17,3 +17,9 @@ timeout 900 python bench.py --sweep --dtype f32 > gpurun_out/${T}_sweep_f32.txt 
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-emitted > gpurun_out/${T}_ncu_launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_tc -s 3 -c 1 -o gpurun_out/${T}_tc python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_tc32 -s 3 -c 1 -o gpurun_out/${T}_tc32 python bench.py --dtype f32 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_full32.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:volume_ltu -s 3 -c 1 -o gpurun_out/${T}_ltu11 python -c "
+import sys, torch; sys.path.insert(0, '.')
+from paper_1604_08501_b200 import DeviceFieldState, volume_rhs_device
+ds = DeviceFieldState.generate(11, 75131, seed=1, dtype=torch.float32)
+for _ in range(5): volume_rhs_device(ds, variant='ltu')
+torch.cuda.synchronize()" > gpurun_out/${T}_ncu_ltu.log 2>&1
