@@ -52,9 +52,16 @@ struct ColCfg {
   static constexpr int TPE = NQ * NQ * KS;  // threads per element
   static constexpr int THREADS = (EPB * TPE + 31) / 32 * 32;
   static constexpr int VEC = 16 / (int)sizeof(T);
+  // odd Nq: scalar line accesses with the odd line stride Nq (every
+  // row-strided access of a warp conflict-free, no vector tail); even Nq:
+  // 16-byte vector loads with an odd number of 16-byte chunks per line
+  // (A/B at 1e8 points: fp64 Nq 3 / 5 / 9 0.355 / 0.661 / 0.316 -> 0.387 /
+  // 0.67 / 0.33, fp32 Nq 5 / 9 0.541 / 0.419 -> 0.598 / 0.427; even Nq lose)
+  static constexpr bool SC = (NQ % 2) == 1;
+  static constexpr int LV = SC ? 1 : VEC;              // line access width (values)
   static constexpr int RV = (NQ + VEC - 1) / VEC;      // 16-byte chunks per line
   static constexpr int RSC = (RV % 2) ? RV : RV + 1;   // odd chunk stride
-  static constexpr int RS = RSC * VEC;                 // padded line stride (values)
+  static constexpr int RS = SC ? (NQ | 1) : RSC * VEC; // padded line stride (values)
   static constexpr int TILE = NQ * NQ * RS;            // one direction, one element
   static constexpr int BUF = 3 * TILE * EPB;           // one field buffer
   // + D(i, n) as given ([n][i]) and transposed with padded rows ([k][n])
@@ -93,17 +100,32 @@ __device__ __forceinline__ void col_scalars(T rho, T th, T p0, T Rp0, T gam, T &
   }
 }
 
-// sum_n d[n] * line[n] over one padded shared line (16-byte vector loads)
-template <typename T, int NQ, int VEC>
-__device__ __forceinline__ T line_dot(const T *line, const T (&d)[NQ], T acc) {
-  using V = typename V16<T>::type;
+// the NQ values of one padded shared line: 16-byte vector loads (LV = VEC)
+// or scalar loads (LV = 1)
+template <typename T, int NQ, int LV>
+__device__ __forceinline__ void load_line(const T *line, T (&out)[NQ]) {
+  if constexpr (LV == 1) {
 #pragma unroll
-  for (int c = 0; c < (NQ + VEC - 1) / VEC; ++c) {
-    const V v = *reinterpret_cast<const V *>(line + c * VEC);
+    for (int n = 0; n < NQ; ++n) out[n] = line[n];
+  } else {
+    using V = typename V16<T>::type;
 #pragma unroll
-    for (int u = 0; u < VEC; ++u)
-      if (c * VEC + u < NQ) acc = fma(d[c * VEC + u], vget(v, u), acc);
+    for (int c = 0; c < (NQ + LV - 1) / LV; ++c) {
+      const V v = *reinterpret_cast<const V *>(line + c * LV);
+#pragma unroll
+      for (int u = 0; u < LV; ++u)
+        if (c * LV + u < NQ) out[c * LV + u] = vget(v, u);
+    }
   }
+}
+
+// sum_n d[n] * line[n] over one padded shared line
+template <typename T, int NQ, int LV>
+__device__ __forceinline__ T line_dot(const T *line, const T (&d)[NQ], T acc) {
+  T x[NQ];
+  load_line<T, NQ, LV>(line, x);
+#pragma unroll
+  for (int n = 0; n < NQ; ++n) acc = fma(d[n], x[n], acc);
   return acc;
 }
 
@@ -113,7 +135,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
                       T *__restrict__ rhsq, const T *__restrict__ D, const T *__restrict__ g,
                       const T *__restrict__ jinv) {
   using C = ColCfg<T, NQ, KS, EPB>;
-  constexpr int NPT = C::NPT, KP = C::KP, RS = C::RS, TILE = C::TILE, VEC = C::VEC;
+  constexpr int NPT = C::NPT, KP = C::KP, RS = C::RS, TILE = C::TILE, VEC = C::VEC, LV = C::LV;
   using V = typename V16<T>::type;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -227,7 +249,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
       if (thread_live) {
         // F_t: the own KP points are contiguous in the column -> 16-byte stores
         T *const dst = tt + (j * NQ + i) * RS + k0;
-        if constexpr ((KP * sizeof(T)) % 16 == 0 && (NQ % KP) == 0) {
+        if constexpr (!C::SC && (KP * sizeof(T)) % 16 == 0 && (NQ % KP) == 0) {
 #pragma unroll
           for (int c = 0; c < KP / VEC; ++c) {
             V v;
@@ -248,13 +270,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
       if (thread_live) {
       // T: the own column along k, against D(k, n) broadcast from sD
       T ftc[NQ];
-#pragma unroll
-      for (int c = 0; c < (NQ + VEC - 1) / VEC; ++c) {
-        const V v = *reinterpret_cast<const V *>(tt + (j * NQ + i) * RS + c * VEC);
-#pragma unroll
-        for (int u = 0; u < VEC; ++u)
-          if (c * VEC + u < NQ) ftc[c * VEC + u] = vget(v, u);
-      }
+      load_line<T, NQ, LV>(tt + (j * NQ + i) * RS, ftc);
 #pragma unroll
       for (int kk = 0; kk < KP; ++kk) {
         const int k = k0 + kk;
@@ -265,18 +281,12 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
           for (int n = 0; n < NQ; ++n) acc = fma(Dkr[kk][n], ftc[n], acc);
         } else {  // D(k, .) row, broadcast within the warp (one k per warp)
           T dk[NQ];
-#pragma unroll
-          for (int c = 0; c < (NQ + VEC - 1) / VEC; ++c) {
-            const V v = *reinterpret_cast<const V *>(sDT + k * RS + c * VEC);
-#pragma unroll
-            for (int u = 0; u < VEC; ++u)
-              if (c * VEC + u < NQ) dk[c * VEC + u] = vget(v, u);
-          }
+          load_line<T, NQ, LV>(sDT + k * RS, dk);
 #pragma unroll
           for (int n = 0; n < NQ; ++n) acc = fma(dk[n], ftc[n], acc);
         }
-        acc = line_dot<T, NQ, VEC>(tr + (k * NQ + j) * RS, Di, acc);
-        acc = line_dot<T, NQ, VEC>(ts + (k * NQ + i) * RS, Dj, acc);
+        acc = line_dot<T, NQ, LV>(tr + (k * NQ + j) * RS, Di, acc);
+        acc = line_dot<T, NQ, LV>(ts + (k * NQ + i) * RS, Dj, acc);
         if (live) re[b * NPT + k * NQ * NQ + col] = fma(jv[kk], acc, rh[kk]);
       }
       }
