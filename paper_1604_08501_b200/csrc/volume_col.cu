@@ -331,9 +331,26 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
   constexpr bool F64 = sizeof(T) == 8;
 #define LFB_L(NQ_, KS_, EPB_, MB_) \
   return launch_col<T, NQ_, KS_, EPB_, MB_>(ne, p0, R, gam, q, rhsq, D, g, jinv, s)
+// A0 = the shipped (KS, EPB, MINB) per Nq; A1, A2 = the measured runners-up
+// (COL_ALT selects one for A/B builds). Re-measured after the odd-Nq scalar
+// lines (1e8 points): fp32 Nq 5 (5,1,8) 0.649 vs (5,2,4) 0.597, fp32 Nq 9
+// (9,1,1) 0.432 vs (3,1,2) 0.426, fp64 Nq 7 (2,1,2) 0.425 vs (7,1,2) 0.377
+#ifndef COL_ALT
+#define COL_ALT 0
+#endif
+#if COL_ALT == 1
+#define LFB_COL3(NQ_, A0, A1, A2) \
+  case NQ_:                       \
+    LFB_L(NQ_, A1);
+#elif COL_ALT == 2
+#define LFB_COL3(NQ_, A0, A1, A2) \
+  case NQ_:                       \
+    LFB_L(NQ_, A2);
+#else
 #define LFB_COL3(NQ_, A0, A1, A2) \
   case NQ_:                       \
     LFB_L(NQ_, A0);
+#endif
   if constexpr (F64) {
     switch (nq) {
       LFB_COL3(2, LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2), LFB_ARGS(1, 32, 2))
@@ -341,7 +358,7 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
       LFB_COL3(4, LFB_ARGS(2, 4, 2), LFB_ARGS(4, 2, 3), LFB_ARGS(1, 8, 2))
       LFB_COL3(5, LFB_ARGS(5, 1, 4), LFB_ARGS(5, 1, 5), LFB_ARGS(5, 1, 6))
       LFB_COL3(6, LFB_ARGS(3, 1, 4), LFB_ARGS(3, 1, 5), LFB_ARGS(6, 1, 4))
-      LFB_COL3(7, LFB_ARGS(7, 1, 2), LFB_ARGS(2, 1, 2), LFB_ARGS(4, 1, 3))
+      LFB_COL3(7, LFB_ARGS(2, 1, 2), LFB_ARGS(7, 1, 2), LFB_ARGS(4, 1, 3))
       LFB_COL3(8, LFB_ARGS(4, 1, 2), LFB_ARGS(8, 1, 1), LFB_ARGS(2, 1, 2))
       LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(9, 1, 1), LFB_ARGS(3, 1, 2))
       LFB_COL3(10, LFB_ARGS(5, 1, 1), LFB_ARGS(10, 1, 1), LFB_ARGS(5, 1, 1))
@@ -354,11 +371,11 @@ int dispatch_col(int nq, int64_t ne, T p0, T R, T gam, const T *q, T *rhsq, cons
       LFB_COL3(2, LFB_ARGS(1, 32, 4), LFB_ARGS(1, 32, 4), LFB_ARGS(1, 32, 4))
       LFB_COL3(3, LFB_ARGS(1, 14, 4), LFB_ARGS(1, 14, 4), LFB_ARGS(1, 14, 4))
       LFB_COL3(4, LFB_ARGS(4, 2, 6), LFB_ARGS(2, 4, 4), LFB_ARGS(1, 8, 4))
-      LFB_COL3(5, LFB_ARGS(5, 2, 4), LFB_ARGS(5, 1, 8), LFB_ARGS(1, 5, 4))
+      LFB_COL3(5, LFB_ARGS(5, 1, 8), LFB_ARGS(5, 2, 4), LFB_ARGS(1, 5, 4))
       LFB_COL3(6, LFB_ARGS(6, 1, 4), LFB_ARGS(3, 1, 6), LFB_ARGS(2, 2, 4))
       LFB_COL3(7, LFB_ARGS(2, 1, 4), LFB_ARGS(7, 1, 4), LFB_ARGS(1, 3, 4))
       LFB_COL3(8, LFB_ARGS(2, 1, 4), LFB_ARGS(4, 1, 4), LFB_ARGS(8, 1, 2))
-      LFB_COL3(9, LFB_ARGS(3, 1, 2), LFB_ARGS(3, 1, 3), LFB_ARGS(9, 1, 1))
+      LFB_COL3(9, LFB_ARGS(9, 1, 1), LFB_ARGS(3, 1, 2), LFB_ARGS(3, 1, 3))
       LFB_COL3(10, LFB_ARGS(2, 1, 2), LFB_ARGS(2, 1, 3), LFB_ARGS(5, 1, 2))
       LFB_COL3(11, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 2), LFB_ARGS(6, 1, 1))
       LFB_COL3(12, LFB_ARGS(4, 1, 1), LFB_ARGS(3, 1, 1), LFB_ARGS(6, 1, 1))
