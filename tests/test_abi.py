@@ -81,3 +81,19 @@ def test_error_mapping_raises_reference_style_exceptions():
         _native.check(_native.LFB_ERR_BAD_NQ)
     with pytest.raises(ExecutionError):
         _native.variant_id("no-such-variant")
+
+
+# LFB_VARIANT_AUTO per (dtype, Nq): the measured winners of the config-5 sweep
+# (profiles/r02_sweep_*.jsonl, DESIGN.md §4 results table)
+AUTO_F64 = {2: "tc", 3: "col", 4: "tc", 5: "col", 6: "tc", 7: "tc", 8: "tc", 9: "lines",
+            10: "lines", 11: "lt", 12: "lt", 13: "lines"}
+AUTO_F32 = {4: "tc", 5: "col", 6: "col", 7: "tc", 8: "tc", 9: "col", 10: "col", 11: "ltu",
+            12: "lt", 13: "tc", 16: "tc"}
+
+
+@pytest.mark.parametrize("nbytes,table", [(8, AUTO_F64), (4, AUTO_F32)])
+def test_auto_resolution_table(nbytes, table):
+    got = {nq: _native.resolve_variant(nbytes, nq) for nq in table}
+    assert got == table
+    for nq, v in table.items():
+        assert _native.variant_available(v, nbytes, nq), (nbytes, nq, v)
