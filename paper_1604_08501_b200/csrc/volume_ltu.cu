@@ -104,7 +104,9 @@ template <int NQ>
 struct LtuCfg {
   static constexpr int NPT = NQ * NQ * NQ;
   static constexpr int NL = NQ * NQ;                // lines per direction (<= 128)
-  static constexpr int P = NQ == 9 ? 3 : NQ == 10 ? 4 : 5;  // points per thread (>= 8 warps)
+  // points per thread: Nq 9, 10 -> 8 warps; Nq 11 -> 7 warps (128 registers at
+  // two CTAs per SM; warp 3 then also reads quadrant 3's second half)
+  static constexpr int P = NQ == 9 ? 3 : NQ == 10 ? 4 : 6;
   static constexpr int THREADS = ((NPT + P - 1) / P + 31) / 32 * 32;
   static constexpr int CRS = 17;                    // exchange-tile row stride (odd)
   static constexpr int SLAB = (NPT + 4 + 3) & ~3;   // stage slab (16-byte aligned superset)
@@ -116,7 +118,8 @@ struct LtuCfg {
                                                   3 * 128 * (size_t)CRS + 5 * (size_t)SLAB) +
                                  6 * sizeof(uint64_t) + 16;
   static_assert(NL <= 128, "one M=128 tile per direction");
-  static_assert(THREADS >= 256, "eight TMEM reader warps");
+  static constexpr int W = THREADS / 32;
+  static_assert(W >= 4, "four TMEM reader warps");
 };
 
 template <int NQ>
@@ -185,6 +188,44 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
     xS[m] = (k * NQ + i) * CRS + j;
     xT[m] = (j * NQ + i) * CRS + k;
   }
+
+  // ---- store rotation: in the warp-wide operand store s of direction d, lane
+  // group g_d(lane) stores its point (s + g_d) mod P instead of point s — the
+  // points of one store then come from several k-planes / lines, so fewer
+  // lanes share a bank (a K-major row keeps a line's K values in four banks).
+  // Bank model over the real patterns, wavefronts per field (hi stores; R+S+T):
+  // Nq 9: 207 -> 153, Nq 10: 281 -> 182, Nq 11: 372 -> 233.
+  const int gR = NQ == 11 ? (lane >> 2) & 3 : (lane >> 1) & 3;
+  const int gS = NQ == 9 ? lane >> 3 : 0;
+  const int gT = lane >> 3;
+  auto rot = [](int s, int gg) { return s + gg < P ? s + gg : s + gg - P; };
+  auto pick_i = [](const int (&a)[P], int m) {
+    int v = a[0];
+#pragma unroll
+    for (int x = 1; x < P; ++x) v = m == x ? a[x] : v;
+    return v;
+  };
+  int oR[P], oS[P], oT[P];
+  uint32_t vR = 0, vS = 0, vT = 0;
+  {
+    int vpi[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) vpi[m] = vp[m] ? 1 : 0;
+#pragma unroll
+    for (int x = 0; x < P; ++x) {
+      oR[x] = pick_i(aR, rot(x, gR));
+      oS[x] = pick_i(aS, rot(x, gS));
+      oT[x] = pick_i(aT, rot(x, gT));
+      vR |= (uint32_t)pick_i(vpi, rot(x, gR)) << x;
+      vS |= (uint32_t)pick_i(vpi, rot(x, gS)) << x;
+      vT |= (uint32_t)pick_i(vpi, rot(x, gT)) << x;
+    }
+  }
+  auto store_split = [&](int d, int off, float v) {
+    const uint32_t hi = ltu_split_hi(v);
+    At[d * AT + off] = __uint_as_float(hi);
+    At[d * AT + off + 96] = v - __uint_as_float(hi);  // K index 12 + n
+  };
 
   // ---- stages (thread 0) ---------------------------------------------------
   auto slab_bytes = [&](const float *a0) {
@@ -295,23 +336,30 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
         const float *gs0 = gst + shift(g + (e * 9 + b - 1) * NPT);
         const float *gs1 = gst + SLAB + shift(g + (e * 9 + 3 + b - 1) * NPT);
         const float *gs2 = gst + 2 * SLAB + shift(g + (e * 9 + 6 + b - 1) * NPT);
+        float fR[P], fS[P], fT[P];
 #pragma unroll
         for (int m = 0; m < P; ++m) {
-          if (!vp[m]) continue;
           const float qv = qs[pt[m]];
-          float f[3] = {Wd[0][m] * qv, Wd[1][m] * qv, Wd[2][m] * qv};
+          fR[m] = Wd[0][m] * qv;
+          fS[m] = Wd[1][m] * qv;
+          fT[m] = Wd[2][m] * qv;
           if (mom) {
-            f[0] = fmaf(gs0[pt[m]], pp[m], f[0]);
-            f[1] = fmaf(gs1[pt[m]], pp[m], f[1]);
-            f[2] = fmaf(gs2[pt[m]], pp[m], f[2]);
+            fR[m] = fmaf(gs0[pt[m]], pp[m], fR[m]);
+            fS[m] = fmaf(gs1[pt[m]], pp[m], fS[m]);
+            fT[m] = fmaf(gs2[pt[m]], pp[m], fT[m]);
           }
-          const int off[3] = {aR[m], aS[m], aT[m]};
+        }
+        auto pick_f = [](const float (&a)[P], int m) {
+          float v = a[0];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const uint32_t hi = ltu_split_hi(f[d]);
-            At[d * AT + off[d]] = __uint_as_float(hi);
-            At[d * AT + off[d] + 96] = f[d] - __uint_as_float(hi);  // K index 12 + n
-          }
+          for (int x = 1; x < P; ++x) v = m == x ? a[x] : v;
+          return v;
+        };
+#pragma unroll
+        for (int x = 0; x < P; ++x) {
+          if ((vR >> x) & 1) store_split(0, oR[x], pick_f(fR, rot(x, gR)));
+          if ((vS >> x) & 1) store_split(1, oS[x], pick_f(fS, rot(x, gS)));
+          if ((vT >> x) & 1) store_split(2, oT[x], pick_f(fT, rot(x, gT)));
         }
       }
       if (p == 6 && tid == 32 && en < ne) {  // next element's phase-1 inputs into L2
@@ -346,30 +394,31 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
         __syncwarp();
         LTU_T(3);
       }
-      // ---- TMEM -> exchange tiles: warps 0..3 take R and T outputs 0..7, warps
-      // 4..7 S and T outputs 8..15 (a warp reads the 32 lanes of quadrant w % 4)
-      if (w < 8) {
-        const int line = 32 * (w & 3) + lane;
-        const uint32_t tq = tmem + ((uint32_t)(32 * (w & 3)) << 16);
-        const int d0 = w < 4 ? 0 : 1;
-        mbar_wait(&bars[3 + d0], mpar);
+      // ---- TMEM -> exchange tiles: half h = 0 (R and T outputs 0..7) or 1 (S and
+      // T outputs 8..15) of quadrant qd (TMEM lanes 32 qd.., readable by warps
+      // with w % 4 == qd): warp qd takes half 0, warp 4 + qd half 1 — or, with
+      // fewer than 8 warps, warp qd both
+      auto read_half = [&](int qd, int h) {
+        const int line = 32 * qd + lane;
+        const uint32_t tq = tmem + ((uint32_t)(32 * qd) << 16);
+        mbar_wait(&bars[3 + h], mpar);
         LTU_T(4);
         asm volatile("tcgen05.fence::after_thread_sync;");
         {  // columns o (X_hi D_hi + X_lo D_hi) and 16 + o (X_hi D_lo)
           uint32_t v[16], u[16];
-          ltu_ld16(v, tq + 32 * d0);
-          ltu_ld16(u, tq + 32 * d0 + 16);
+          ltu_ld16(v, tq + 32 * h);
+          ltu_ld16(u, tq + 32 * h + 16);
           if (line < C::NL) {
 #pragma unroll
             for (int o = 0; o < NQ; ++o)
-              Xc[(d0 * 128 + line) * CRS + o] = __uint_as_float(v[o]) + __uint_as_float(u[o]);
+              Xc[(h * 128 + line) * CRS + o] = __uint_as_float(v[o]) + __uint_as_float(u[o]);
           }
         }
         mbar_wait(&bars[5], mpar);
         LTU_T(5);
         asm volatile("tcgen05.fence::after_thread_sync;");
         {
-          const int o0 = w < 4 ? 0 : 8;
+          const int o0 = 8 * h;
           uint32_t v[8], u[8];
           ltu_ld8(v, tq + 64 + o0);
           ltu_ld8(u, tq + 80 + o0);
@@ -380,6 +429,10 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
                 Xc[(256 + line) * CRS + o0 + o] = __uint_as_float(v[o]) + __uint_as_float(u[o]);
           }
         }
+      };
+      if (w < 8) {
+        read_half(w & 3, w >> 2);
+        if (w < 4 && w + 4 >= C::W) read_half(w, 1);
         asm volatile("tcgen05.fence::before_thread_sync;");
       }
       mpar ^= 1u;
