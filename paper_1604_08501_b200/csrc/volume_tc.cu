@@ -166,7 +166,14 @@ __device__ __forceinline__ void st_pair(T *p, double a, double b) {
 //   stile per-warp [j][i], row stride 12 (96 B): the in-plane S transpose.
 constexpr int FT_PS = 68, FT_FS = 8 * FT_PS;
 constexpr int TO_PS = 72, TO_FS = 8 * TO_PS;
-constexpr int ST_RS = 12, ST_SZ = 8 * ST_RS;
+constexpr int ST_SZ = 72;
+// row r of the per-warp F_s transpose tile (8 rows x 8 doubles): the 16-byte
+// pair stores (rows gq, 2a / 2a+1 per quarter-warp) and the transposed 8-byte
+// reads (rows c + 4t, column gq per half-warp) are both conflict-free with
+// these row starts (a plain stride of 12 made the stores 2-way)
+__device__ __forceinline__ int st_row(int r) {
+  return 8 * r + 4 * (((r >> 1) & 1) + ((r >> 2) & 1));
+}
 
 // NW < 8 (zero-padded Nq, one warp per real k-plane): stages hold the real
 // q + g slab only (+ the g superset's 16-byte shift)
@@ -460,12 +467,12 @@ __global__ void __launch_bounds__(32 * NW, 1)
         }
       }
       double *stl = sm.stile[w][b & 1];
-      sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
+      sts2(stl + st_row(gq) + 2 * c, fs[0], fs[1]);
       if (MUT != 3) __syncwarp();
       double fsT[2], ftQ[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
+        fsT[t] = stl[st_row(c + 4 * t) + gq];
         ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
       }
       double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
@@ -748,12 +755,12 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       }
       double *stl = alias + LEAN_STILE + w * ST_SZ;
       if (b > 0) __syncwarp();  // previous field's transposed reads are done
-      sts2(stl + gq * ST_RS + 2 * c, fs[0], fs[1]);
+      sts2(stl + st_row(gq) + 2 * c, fs[0], fs[1]);
       __syncwarp();
       double fsT[2], ftQ[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        fsT[t] = stl[(c + 4 * t) * ST_RS + gq];
+        fsT[t] = stl[st_row(c + 4 * t) + gq];
         ftQ[t] = sm.ft[b * FT_FS + ftR[t]];
       }
       double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
