@@ -58,10 +58,14 @@ struct ColCfg {
   // (A/B at 1e8 points: fp64 Nq 3 / 5 / 9 0.355 / 0.661 / 0.316 -> 0.387 /
   // 0.67 / 0.33, fp32 Nq 5 / 9 0.541 / 0.419 -> 0.598 / 0.427; even Nq lose)
   static constexpr bool SC = (NQ % 2) == 1;
-  static constexpr int LV = SC ? 1 : VEC;              // line access width (values)
+  // fp32 Nq = 2 mod 4: 8-byte line accesses with an odd number of 8-byte units
+  // per line (a 16-byte chunk stride leaves a 2-float tail whose 8-byte reads
+  // conflict 2-4 ways): Nq 6 / 10 0.596 / 0.424 -> 0.627 / 0.476
+  static constexpr bool S2 = sizeof(T) == 4 && NQ % 4 == 2;
+  static constexpr int LV = SC ? 1 : S2 ? 2 : VEC;    // line access width (values)
   static constexpr int RV = (NQ + VEC - 1) / VEC;      // 16-byte chunks per line
   static constexpr int RSC = (RV % 2) ? RV : RV + 1;   // odd chunk stride
-  static constexpr int RS = SC ? (NQ | 1) : RSC * VEC; // padded line stride (values)
+  static constexpr int RS = SC ? (NQ | 1) : S2 ? ((NQ / 2) % 2 ? NQ : NQ + 2) : RSC * VEC;
   static constexpr int TILE = NQ * NQ * RS;            // one direction, one element
   static constexpr int BUF = 3 * TILE * EPB;           // one field buffer
   // + D(i, n) as given ([n][i]) and transposed with padded rows ([k][n])
@@ -107,6 +111,13 @@ __device__ __forceinline__ void load_line(const T *line, T (&out)[NQ]) {
   if constexpr (LV == 1) {
 #pragma unroll
     for (int n = 0; n < NQ; ++n) out[n] = line[n];
+  } else if constexpr (LV == 2 && sizeof(T) == 4) {  // pairs of floats
+#pragma unroll
+    for (int c = 0; c < NQ / 2; ++c) {
+      const float2 v = *reinterpret_cast<const float2 *>(line + 2 * c);
+      out[2 * c] = v.x;
+      out[2 * c + 1] = v.y;
+    }
   } else {
     using V = typename V16<T>::type;
 #pragma unroll
@@ -249,7 +260,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
       if (thread_live) {
         // F_t: the own KP points are contiguous in the column -> 16-byte stores
         T *const dst = tt + (j * NQ + i) * RS + k0;
-        if constexpr (!C::SC && (KP * sizeof(T)) % 16 == 0 && (NQ % KP) == 0) {
+        if constexpr (!C::SC && !C::S2 && (KP * sizeof(T)) % 16 == 0 && (NQ % KP) == 0) {
 #pragma unroll
           for (int c = 0; c < KP / VEC; ++c) {
             V v;
