@@ -572,6 +572,10 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
   const double Rp0 = R / p0;
 
   constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
+  // even padded Nq (6): a lane's two points are valid together and 16-byte
+  // aligned, so they move as one 16-byte access (the separate 8-byte stage
+  // reads were 2-3-way bank conflicted)
+  constexpr bool PAIRS = PAD && SUB % 2 == 0;
   constexpr int P = PAD ? 1 : 8 / SUB, NPTR = SUB * SUB * SUB;
   constexpr int SLABQ = PAD ? 8 * NPTR : 8 * TC_NPT;
   constexpr int SLABG = PAD ? 9 * NPTR : 9 * TC_NPT;
@@ -658,9 +662,11 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
                   (PAD ? (reinterpret_cast<uintptr_t>(g + e * SLABG) & 15) / sizeof(T) : 0);
     T *re = rhsq + e * SLABQ;
     double jv[2];
-    if (PAD) {
+    if (PAD && !PAIRS) {
       jv[0] = vld[0] ? (double)jinv[e * SLABJ + jo] : 0.0;
       jv[1] = vld[1] ? (double)jinv[e * SLABJ + jo + 1] : 0.0;
+    } else if (PAIRS && !vld[0]) {
+      jv[0] = jv[1] = 0.0;
     } else {
       ldg_pair(jinv + e * SLABJ + jo, jv[0], jv[1]);
     }
@@ -673,18 +679,22 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       double qv[8][2], gv[9][2];
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
-        if (PAD) {
+        if (PAD && !PAIRS) {
           qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
           qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
+        } else if (PAIRS && !vld[0]) {
+          qv[f][0] = qv[f][1] = (f == 0 ? 1.0 : 0.0);
         } else {
           ld_pair(sq + qo + f * NPTR, qv[f][0], qv[f][1]);
         }
       }
 #pragma unroll
       for (int x = 0; x < 9; ++x) {
-        if (PAD) {
+        if (PAD && !PAIRS) {
           gv[x][0] = vld[0] ? (double)sg[go + x * NPTR] : 0.0;
           gv[x][1] = vld[1] ? (double)sg[go + x * NPTR + 1] : 0.0;
+        } else if (PAIRS && !vld[0]) {
+          gv[x][0] = gv[x][1] = 0.0;
         } else {
           ld_pair(sg + go + x * NPTR, gv[x][0], gv[x][1]);
         }
@@ -725,9 +735,11 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
     // ---- phase 2: per field, written back as soon as T is exchanged ------
     // (rhsq of field b+1 is loaded while field b computes)
     auto ld_rh = [&](int b, double &r0, double &r1) {
-      if (PAD) {
+      if (PAD && !PAIRS) {
         r0 = vld[0] ? (double)re[qo + b * NPTR] : 0.0;
         r1 = vld[1] ? (double)re[qo + b * NPTR + 1] : 0.0;
+      } else if (PAIRS && !vld[0]) {
+        r0 = r1 = 0.0;
       } else {
         ld_pair(re + qo + b * NPTR, r0, r1);
       }
@@ -776,10 +788,10 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
       const double2 t = *reinterpret_cast<const double2 *>(tout + toR);
       const double o0 = rh0 + jv[0] * (a0 + t.x);
       const double o1 = rh1 + jv[1] * (a1 + t.y);
-      if (PAD) {
+      if (PAD && !PAIRS) {
         if (vld[0]) re[qo + b * NPTR] = (T)o0;
         if (vld[1]) re[qo + b * NPTR + 1] = (T)o1;
-      } else {
+      } else if (!PAIRS || vld[0]) {
         st_pair(re + qo + b * NPTR, o0, o1);
       }
     }
