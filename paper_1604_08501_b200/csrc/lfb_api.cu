@@ -71,7 +71,8 @@ int resolve(int variant, int bytes, int nq) {
   if (variant == LFB_VARIANT_AUTO) {
     // measured on B200 (profiles/r01_sweep_*.jsonl, profiles/r01_col_sweep_*.jsonl,
     // profiles/r02_*):
-    // col wins where tc pads most of its virtual Nq=8 cube (Nq 5, 6) and
+    // col wins where tc pads most of its virtual Nq=8 cube (Nq 5; Nq 6 went
+    // to the per-plane tc schedule with paired accesses in round 2) and
     // for fp32 above Nq = 8 (FFMA vs the fp64 DMMA line GEMMs); tc keeps
     // Nq 2, 4, 7, 8 and fp32 Nq 13..16 (the 16x16-plane TF32 kernel); lines
     // keeps fp64 Nq 9..13 (profiles/r01_col_configs.txt, r01_tc16.txt)
@@ -81,7 +82,7 @@ int resolve(int variant, int bytes, int nq) {
     if (nq == 11 && lfb::ltu_available(bytes, nq)) return LFB_VARIANT_LTU;
     if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::col_available(bytes, nq)) {
-      if (nq == 5 || (nq == 6 && bytes == 4)) return LFB_VARIANT_COL;
+      if (nq == 5) return LFB_VARIANT_COL;
       if (bytes == 4 && nq >= 9 && nq <= 12) return LFB_VARIANT_COL;
       if (bytes == 8 && nq == 3) return LFB_VARIANT_COL;
     }

@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
   // SUB = real Nq: 8 one element per group; 4 / 2 pack (8/SUB)^3 elements
   // into a virtual Nq=8 cube with blockdiag D; 5..7 zero-pad one element
   constexpr bool PAD = !(SUB == 8 || SUB == 4 || SUB == 2);
+  // even padded Nq (6): a lane's two points are valid together and 8-byte
+  // aligned -> one 8-byte access (as volume_tc.cu)
+  constexpr bool PAIRS = PAD && SUB % 2 == 0;
   static_assert(SUB >= 2 && SUB <= 8, "virtual Nq=8 cube");
   constexpr int P = PAD ? 1 : 8 / SUB, NPTR = SUB * SUB * SUB;
   constexpr int SLABQ = PAD ? 8 * NPTR : 8 * NPT8;
@@ -284,18 +287,22 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
     float rh[8][2], jv[2];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      if (PAD) {
+      if (PAD && !PAIRS) {
         rh[b][0] = vld[0] ? re[qo + b * NPTR] : 0.0f;
         rh[b][1] = vld[1] ? re[qo + b * NPTR + 1] : 0.0f;
+      } else if (PAIRS && !vld[0]) {
+        rh[b][0] = rh[b][1] = 0.0f;
       } else {
         const float2 v = *reinterpret_cast<const float2 *>(re + qo + b * NPTR);
         rh[b][0] = v.x;
         rh[b][1] = v.y;
       }
     }
-    if (PAD) {
+    if (PAD && !PAIRS) {
       jv[0] = vld[0] ? jinv[e * SLABJ + jo] : 0.0f;
       jv[1] = vld[1] ? jinv[e * SLABJ + jo + 1] : 0.0f;
+    } else if (PAIRS && !vld[0]) {
+      jv[0] = jv[1] = 0.0f;
     } else {
       const float2 v = __ldg(reinterpret_cast<const float2 *>(jinv + e * SLABJ + jo));
       jv[0] = v.x;
@@ -311,9 +318,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
       float qv[8][2], gv[9][2];
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
-        if (PAD) {
+        if (PAD && !PAIRS) {
           qv[f][0] = vld[0] ? sq[sqo + f * NPTR] : (f == 0 ? 1.0f : 0.0f);
           qv[f][1] = vld[1] ? sq[sqo + f * NPTR + 1] : (f == 0 ? 1.0f : 0.0f);
+        } else if (PAIRS && !vld[0]) {
+          qv[f][0] = qv[f][1] = (f == 0 ? 1.0f : 0.0f);
         } else {
           const float2 v = *reinterpret_cast<const float2 *>(sq + sqo + f * NPTR);
           qv[f][0] = v.x;
@@ -322,9 +331,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
       }
 #pragma unroll
       for (int x = 0; x < 9; ++x) {
-        if (PAD) {
+        if (PAD && !PAIRS) {
           gv[x][0] = vld[0] ? sg[go + x * NPTR] : 0.0f;
           gv[x][1] = vld[1] ? sg[go + x * NPTR + 1] : 0.0f;
+        } else if (PAIRS && !vld[0]) {
+          gv[x][0] = gv[x][1] = 0.0f;
         } else {
           const float2 v = *reinterpret_cast<const float2 *>(sg + go + x * NPTR);
           gv[x][0] = v.x;
@@ -413,10 +424,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
       const float2 t = *reinterpret_cast<const float2 *>(sm.tout + b * TO_FS + toR);
       const float o0 = fmaf(jv[0], acc[b][0] + t.x, rh[b][0]);
       const float o1 = fmaf(jv[1], acc[b][1] + t.y, rh[b][1]);
-      if (PAD) {
+      if (PAD && !PAIRS) {
         if (vld[0]) re[qo + b * NPTR] = o0;
         if (vld[1]) re[qo + b * NPTR + 1] = o1;
-      } else {
+      } else if (!PAIRS || vld[0]) {
         *reinterpret_cast<float2 *>(re + qo + b * NPTR) = make_float2(o0, o1);
       }
     }
