@@ -128,7 +128,7 @@ struct LinesGeom {
   // MODE 0 line stride: odd, except Nq = 10 where the even stride 10 puts the
   // B-fragment reads, C-fragment writes and owner accesses on fewer
   // conflicted wavefronts (bank model 490 -> 424 / 466 -> 377 per element
-  // field; measured 0.467 -> 0.483 of HBM)
+  // field, tools/lines_banks.py; measured 0.467 -> 0.483 of HBM)
   static constexpr int LS0 = NQ == 10 ? 10 : (NQ | 1);
   static constexpr int LSF = MODE == 0 ? LS0 : stride_mod16(NQ, 4, 12);
   static constexpr int LSA = MODE == 0 ? LS0 : stride_mod16(NQ, 2, 2);

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(LtuCfg<NQ>::THREADS, 2)
   // points of one store then come from several k-planes / lines, so fewer
   // lanes share a bank (a K-major row keeps a line's K values in four banks).
   // Bank model over the real patterns, wavefronts per field (hi stores; R+S+T):
-  // Nq 9: 207 -> 153, Nq 10: 281 -> 182, Nq 11: 372 -> 233.
+  // Nq 9: 207 -> 153, Nq 10: 281 -> 182, Nq 11: 372 -> 247 (tools/ltu_banks.py).
   const int gR = NQ == 11 ? (lane >> 2) & 3 : (lane >> 1) & 3;
   const int gS = NQ == 9 ? lane >> 3 : 0;
   const int gT = lane >> 3;
