@@ -614,6 +614,7 @@ def run_sweep(args) -> None:
     inputs, kernel time only, one JSON line per Nq (--variant forces one)."""
     import torch
     from paper_1604_08501_b200 import DeviceFieldState, _native, volume_rhs_device
+    from paper_1604_08501_b200.telemetry import ClockSampler
     torch.cuda.set_device(0)
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     nbytes = 8 if dt == torch.float64 else 4
@@ -626,8 +627,9 @@ def run_sweep(args) -> None:
             variant = args.variant
         s = torch.cuda.current_stream()
         steps = max(3, min(args.steps, 50))
-        _, ms = time_launches(lambda: volume_rhs_device(ds, variant=variant), s, steps,
-                              max(args.warmup, 1))
+        with ClockSampler(0) as clk:
+            _, ms = time_launches(lambda: volume_rhs_device(ds, variant=variant), s, steps,
+                                  max(args.warmup, 1))
         pts = nq ** 3 * ne
         gbs = bytes_per_point(nbytes) * pts / (ms * 1e-3) / 1e9
         print(json.dumps({"sweep": True, "metric": METRIC.replace("Nq=8", f"Nq={nq}"),
@@ -635,7 +637,8 @@ def run_sweep(args) -> None:
                           "variant": variant, "ms_per_launch": ms,
                           "value": pts / (ms * 1e-3) / 1e9, "unit": UNIT,
                           "hbm_gbs": gbs, "frac": gbs / peak, "peak": peak,
-                          "peak_source": peak_src, "steps": steps}), flush=True)
+                          "peak_source": peak_src, "steps": steps,
+                          "clocks": clk.summary()}), flush=True)
         del ds
         torch.cuda.empty_cache()
 
