@@ -589,6 +589,19 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
   bool vld[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) vld[s] = !PAD || (2 * c + s < SUB && gq < SUB && w < SUB);
+  // odd padded Nq: the two 8-byte stage reads of a lane's point pair go out
+  // in a per-lane order (bit = point 2c+1 first) chosen by exhaustive search
+  // so that both instructions are conflict-free (Nq 7: 2-way -> none; Nq 5
+  // is conflict-free either way); a uniform shift (plane, field, g offset)
+  // does not change the bank pattern, so one mask serves every read
+  const int sw = (PAD && !PAIRS && SUB == 7) ? (int)((0x70873u >> lane) & 1u) : 0;
+  auto ld_stage = [&](const T *p, double dflt, double &a, double &b) {
+    const bool v0 = vld[sw], v1 = vld[sw ^ 1];
+    const double x0 = v0 ? (double)p[sw] : dflt;
+    const double x1 = v1 ? (double)p[sw ^ 1] : dflt;
+    a = sw ? x1 : x0;
+    b = sw ? x0 : x1;
+  };
   const int ftW = w * FT_PS + gq * 8 + 2 * c;
   const int toR = w * TO_PS + gq * 8 + 2 * c;
   const int toW = gq * TO_PS + w * 8 + 2 * c;
@@ -680,8 +693,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         if (PAD && !PAIRS) {
-          qv[f][0] = vld[0] ? (double)sq[qo + f * NPTR] : (f == 0 ? 1.0 : 0.0);
-          qv[f][1] = vld[1] ? (double)sq[qo + f * NPTR + 1] : (f == 0 ? 1.0 : 0.0);
+          ld_stage(sq + qo + f * NPTR, f == 0 ? 1.0 : 0.0, qv[f][0], qv[f][1]);
         } else if (PAIRS && !vld[0]) {
           qv[f][0] = qv[f][1] = (f == 0 ? 1.0 : 0.0);
         } else {
@@ -691,8 +703,7 @@ __global__ void __launch_bounds__(32 * NW, (TcLeanCfg<T, SUB, NW>::MINB))
 #pragma unroll
       for (int x = 0; x < 9; ++x) {
         if (PAD && !PAIRS) {
-          gv[x][0] = vld[0] ? (double)sg[go + x * NPTR] : 0.0;
-          gv[x][1] = vld[1] ? (double)sg[go + x * NPTR + 1] : 0.0;
+          ld_stage(sg + go + x * NPTR, 0.0, gv[x][0], gv[x][1]);
         } else if (PAIRS && !vld[0]) {
           gv[x][0] = gv[x][1] = 0.0;
         } else {

@@ -200,6 +200,17 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
   bool vld[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) vld[s] = !PAD || (2 * c + s < SUB && gq < SUB && w < SUB);
+  // odd padded Nq: per-lane order of the two 4-byte stage reads of a point
+  // pair, searched so both instructions are conflict-free (Nq 7; as
+  // volume_tc.cu)
+  const int sw = (PAD && !PAIRS && SUB == 7) ? (int)((0x38b4b11eu >> lane) & 1u) : 0;
+  auto ld_stage = [&](const float *p, float dflt, float &a, float &b) {
+    const bool v0 = vld[sw], v1 = vld[sw ^ 1];
+    const float x0 = v0 ? p[sw] : dflt;
+    const float x1 = v1 ? p[sw ^ 1] : dflt;
+    a = sw ? x1 : x0;
+    b = sw ? x0 : x1;
+  };
   const int ftW = w * FT_PS + gq * 8 + 2 * c;
   const int toR = w * TO_PS + gq * 8 + 2 * c;
   const int toW = gq * TO_PS + w * 8 + 2 * c;
@@ -319,8 +330,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         if (PAD && !PAIRS) {
-          qv[f][0] = vld[0] ? sq[sqo + f * NPTR] : (f == 0 ? 1.0f : 0.0f);
-          qv[f][1] = vld[1] ? sq[sqo + f * NPTR + 1] : (f == 0 ? 1.0f : 0.0f);
+          ld_stage(sq + sqo + f * NPTR, f == 0 ? 1.0f : 0.0f, qv[f][0], qv[f][1]);
         } else if (PAIRS && !vld[0]) {
           qv[f][0] = qv[f][1] = (f == 0 ? 1.0f : 0.0f);
         } else {
@@ -332,8 +342,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? (NS == 2 ? 2 : 1) : (SUB <=
 #pragma unroll
       for (int x = 0; x < 9; ++x) {
         if (PAD && !PAIRS) {
-          gv[x][0] = vld[0] ? sg[go + x * NPTR] : 0.0f;
-          gv[x][1] = vld[1] ? sg[go + x * NPTR + 1] : 0.0f;
+          ld_stage(sg + go + x * NPTR, 0.0f, gv[x][0], gv[x][1]);
         } else if (PAIRS && !vld[0]) {
           gv[x][0] = gv[x][1] = 0.0f;
         } else {
