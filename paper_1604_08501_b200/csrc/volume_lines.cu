@@ -167,9 +167,23 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
   auto ld2 = [&](const T *p) -> double { return hint ? (double)ldh(p, drop) : (double)__ldg(p); };
 
   // A fragments: A[g][c] = D(pos = 8 mt + g, n = 4 ks + c), zero outside [0,NQ)
-  double Da[MT][KS];
+  // Nq 9: the second output tile would hold 1 valid position of 8 — it goes
+  // to the DFMA pipe instead (from the B fragment each lane already holds,
+  // reduced over the 4 lanes of a line): 0.424 -> 0.431 of HBM. (Nq 10's two
+  // tail positions spill at 128 registers and lose: 0.483 -> 0.447.)
+  constexpr int TAIL = (MT == 2 && NQ == 9) ? 1 : 0;
+  constexpr int MTD = TAIL ? 1 : MT;  // output tiles on the tensor pipe
+  double Dt[TAIL ? TAIL : 1][KS];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
+  for (int r = 0; r < TAIL; ++r)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int n = 4 * ks + c;
+      Dt[r][ks] = n < NQ ? (double)__ldg(D + n * NQ + 8 + r) : 0.0;
+    }
+  double Da[MTD][KS];
+#pragma unroll
+  for (int mt = 0; mt < MTD; ++mt)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int pos = 8 * mt + gq, n = 4 * ks + c;
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
         }
         const int l0 = 8 * lt + 2 * c;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
+        for (int mt = 0; mt < MTD; ++mt) {
           double c0 = 0.0, c1 = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) dmma_ln(c0, c1, Da[mt][ks], bv[ks]);
@@ -301,6 +315,18 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
             if (l0 < NL) ad[l0 * LSA + pos] = c0;
             if (l0 + 1 < NL) ad[(l0 + 1) * LSA + pos] = c1;
           }
+        }
+        if constexpr (TAIL > 0) {
+          double ts[TAIL];
+#pragma unroll
+          for (int r = 0; r < TAIL; ++r) {
+            ts[r] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) ts[r] = fma(Dt[r][ks], bv[ks], ts[r]);
+            ts[r] += __shfl_xor_sync(0xffffffffu, ts[r], 1);
+            ts[r] += __shfl_xor_sync(0xffffffffu, ts[r], 2);
+          }
+          if (c < TAIL && lineB < NL) ad[lineB * LSA + 8 + c] = c == 0 ? ts[0] : ts[TAIL - 1];
         }
       }
       __syncthreads();
