@@ -293,8 +293,15 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
       __syncthreads();
 
       // ---- line GEMMs on the fp64 tensor pipe -----------------------------
-      for (int t = warp; t < 3 * LT; t += LN_THREADS / 32) {
-        const int d = t / LT, lt = t % LT;
+      // NL = 8 m + 1 (Nq 9, 13): the last line tile of each direction holds
+      // one line — it goes to the DFMA pipe on the warps with the fewest
+      // tiles instead of costing a full DMMA tile job (Nq 9 / 13: 0.431 /
+      // 0.299 -> 0.458 / 0.328 of HBM; Nq 11, whose 16 warps were balanced,
+      // lost 0.444 -> 0.424 and keeps the tile)
+      constexpr bool LONE = NL % 8 == 1 && NQ != 11;
+      constexpr int LTJ = LONE ? LT - 1 : LT;  // DMMA line tiles per direction
+      for (int t = warp; t < 3 * LTJ; t += LN_THREADS / 32) {
+        const int d = t / LTJ, lt = t % LTJ;
         const double *fd = fl + d * TSF;
         double *ad = ac + d * TSA;
         const int lineB = 8 * lt + gq;  // B column = line
@@ -327,6 +334,20 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
             ts[r] += __shfl_xor_sync(0xffffffffu, ts[r], 2);
           }
           if (c < TAIL && lineB < NL) ad[lineB * LSA + 8 + c] = c == 0 ? ts[0] : ts[TAIL - 1];
+        }
+      }
+      if constexpr (LONE) {  // line NL - 1 of direction d: lane o computes output o
+        constexpr int NW = LN_THREADS / 32;
+        const int d = warp == NW - 1 ? 1 : warp == NW - 2 ? 0 : -1;
+#pragma unroll 1
+        for (int dd = d; dd >= 0 && dd < 3; dd += 2) {
+          const double *fd = fl + dd * TSF + (NL - 1) * LSF;
+          if (lane < NQ) {
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < NQ; ++n) acc = fma((double)__ldg(D + n * NQ + lane), fd[n], acc);
+            ac[dd * TSA + (NL - 1) * LSA + lane] = acc;
+          }
         }
       }
       __syncthreads();
