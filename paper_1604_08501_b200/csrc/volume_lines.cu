@@ -118,6 +118,21 @@ constexpr int stride_mod16(int nq, int r1, int r2) {
 //     stride = 2 mod 16 -> {4c + g} distinct.
 // (profiles/r01_lines_banks.txt: MODE 0 makes a third of the shared
 // wavefronts bank-conflict replays, but MODE 1 is slower — see launch_lines.)
+// contraction index n held by lane column c at k-step ks of a line GEMM: the
+// order of the K dimension is free (A = D fragments and B = flux fragments
+// use the same map), so at Nq 9 it is permuted to make the B-fragment reads
+// of 4 consecutive lines hit distinct banks (exhaustive search over the K
+// partitions with the half-warp bank model: 2-way -> none; 0.458 -> 0.465
+// of HBM); -1 = padding
+__device__ __forceinline__ int lines_kidx(int nq, int ks, int c) {
+  // packed 4-bit tables (15 = padding), one nibble per (ks, c)
+  // (Nq 10's best map, 0xFF7654329810, measured slower: 0.483 -> 0.473)
+  const uint64_t t = nq == 9 ? 0xF763F852F410ull : 0;
+  if (t == 0) return 4 * ks + c;
+  const int v = (int)((t >> (4 * (4 * ks + c))) & 15);
+  return v == 15 ? -1 : v;
+}
+
 template <int NQ, int MODE, int TH = LinesCfg<NQ>::THREADS>
 struct LinesGeom {
   static constexpr int NPT = NQ * NQ * NQ;
@@ -178,16 +193,16 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
   for (int r = 0; r < TAIL; ++r)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const int n = 4 * ks + c;
-      Dt[r][ks] = n < NQ ? (double)__ldg(D + n * NQ + 8 + r) : 0.0;
+      const int n = lines_kidx(NQ, ks, c);
+      Dt[r][ks] = (n >= 0 && n < NQ) ? (double)__ldg(D + n * NQ + 8 + r) : 0.0;
     }
   double Da[MTD][KS];
 #pragma unroll
   for (int mt = 0; mt < MTD; ++mt)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const int pos = 8 * mt + gq, n = 4 * ks + c;
-      Da[mt][ks] = (pos < NQ && n < NQ) ? (double)__ldg(D + n * NQ + pos) : 0.0;
+      const int pos = 8 * mt + gq, n = lines_kidx(NQ, ks, c);
+      Da[mt][ks] = (pos < NQ && n >= 0 && n < NQ) ? (double)__ldg(D + n * NQ + pos) : 0.0;
     }
 
   for (int64_t e = blockIdx.x; e < ne; e += gridDim.x) {
@@ -308,8 +323,8 @@ __global__ void __launch_bounds__(TH, (TH == LinesCfg<NQ>::THREADS) ? LinesCfg<N
         double bv[KS];                  // shared by every output-position tile
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          const int n = 4 * ks + c;
-          bv[ks] = (lineB < NL && n < NQ) ? fd[lineB * LSF + n] : 0.0;
+          const int n = lines_kidx(NQ, ks, c);
+          bv[ks] = (lineB < NL && n >= 0 && n < NQ) ? fd[lineB * LSF + n] : 0.0;
         }
         const int l0 = 8 * lt + 2 * c;
 #pragma unroll
