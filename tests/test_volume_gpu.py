@@ -326,3 +326,21 @@ def test_line_tile_kernels_many_elements_against_c_oracle(cuda_device, nq, ne):
             got = ds.rhsq.to(torch.float64).cpu().numpy()
             err = max_rel_error(coracle.from_element_batched(got), want)
             assert err <= tol, (v, dtype, err)
+
+
+@pytest.mark.parametrize("nq,ne", [(5, 1301), (6, 977), (7, 611), (9, 523), (10, 409), (13, 151)])
+def test_padded_column_and_lines_kernels_many_elements(cuda_device, nq, ne):
+    """The per-plane tc schedule (paired / reordered stage reads at Nq 6, 7),
+    the column kernel's Nq-parity line layouts, and the lines kernel's tail
+    outputs, one-line tiles and permuted contraction order — over more
+    elements than resident CTAs, against the C oracle."""
+    st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=nq + 23))
+    q, g, j, d = coracle.to_element_batched(st)
+    want = coracle.from_element_batched(coracle.volume_f64_eb(nq, q, g, j, d, st.constants))
+    for dtype, nbytes, tol in ((torch.float64, 8, TOL64), (torch.float32, 4, TOL32)):
+        for v in [x for x in ("tc", "col", "lines") if _native.variant_available(x, nbytes, nq)]:
+            ds = DeviceFieldState.from_field_state(st, dtype=dtype)
+            volume_rhs_device(ds, variant=v)
+            got = ds.rhsq.to(torch.float64).cpu().numpy()
+            err = max_rel_error(coracle.from_element_batched(got), want)
+            assert err <= tol, (v, dtype, err)
