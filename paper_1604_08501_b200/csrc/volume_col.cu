@@ -66,8 +66,16 @@ struct ColCfg {
   static constexpr int RV = (NQ + VEC - 1) / VEC;      // 16-byte chunks per line
   static constexpr int RSC = (RV % 2) ? RV : RV + 1;   // odd chunk stride
   static constexpr int RS = SC ? (NQ | 1) : S2 ? ((NQ / 2) % 2 ? NQ : NQ + 2) : RSC * VEC;
-  static constexpr int TILE = NQ * NQ * RS;            // one direction, one element
-  static constexpr int BUF = 3 * TILE * EPB;           // one field buffer
+  // per-direction line strides: RS, except where the bank model of the
+  // scalar patterns (tools/col_banks.py) finds a better one for the F_s rows
+  // / F_t columns: fp64 Nq 5 F_s 13, F_t 9 (0.676 -> 0.686 of HBM)
+  static constexpr bool ALT5 = SC && sizeof(T) == 8 && NQ == 5;
+  static constexpr int RSS = ALT5 ? 13 : RS, RST = ALT5 ? 9 : RS;
+  static constexpr int TILE = NQ * NQ * RS;            // F_r, one element
+  static constexpr int TILES = NQ * NQ * RSS;          // F_s
+  static constexpr int TILET = NQ * NQ * RST;          // F_t
+  static constexpr int ETILE = TILE + TILES + TILET;   // one element, three directions
+  static constexpr int BUF = ETILE * EPB;              // one field buffer
   // + D(i, n) as given ([n][i]) and transposed with padded rows ([k][n])
   static constexpr size_t smem() { return sizeof(T) * (2 * BUF + NQ * NQ + NQ * RS); }
 };
@@ -187,9 +195,9 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
   }
   // own points' offsets inside an element slab, and tile positions
   const int col = j * NQ + i;
-  T *const tr0 = sbuf + (slot * 3 + 0) * TILE;  // F_r rows (k, j) along i
-  T *const ts0 = sbuf + (slot * 3 + 1) * TILE;  // F_s rows (k, i) along j
-  T *const tt0 = sbuf + (slot * 3 + 2) * TILE;  // F_t columns (j, i) along k
+  T *const tr0 = sbuf + slot * C::ETILE;                 // F_r rows (k, j) along i
+  T *const ts0 = tr0 + TILE;                              // F_s rows (k, i) along j
+  T *const tt0 = ts0 + C::TILES;                          // F_t columns (j, i) along k
 
   int buf = 0;
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
@@ -254,12 +262,12 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
           }
         }
         tr[(k * NQ + j) * RS + i] = fr;
-        ts[(k * NQ + i) * RS + j] = fs;
+        ts[(k * NQ + i) * C::RSS + j] = fs;
         ftv[kk] = ft;
       }
       if (thread_live) {
         // F_t: the own KP points are contiguous in the column -> 16-byte stores
-        T *const dst = tt + (j * NQ + i) * RS + k0;
+        T *const dst = tt + (j * NQ + i) * C::RST + k0;
         if constexpr (!C::SC && !C::S2 && (KP * sizeof(T)) % 16 == 0 && (NQ % KP) == 0) {
 #pragma unroll
           for (int c = 0; c < KP / VEC; ++c) {
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
       if (thread_live) {
       // T: the own column along k, against D(k, n) broadcast from sD
       T ftc[NQ];
-      load_line<T, NQ, LV>(tt + (j * NQ + i) * RS, ftc);
+      load_line<T, NQ, LV>(tt + (j * NQ + i) * C::RST, ftc);
 #pragma unroll
       for (int kk = 0; kk < KP; ++kk) {
         const int k = k0 + kk;
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(ColCfg<T, NQ, KS, EPB>::THREADS, MINB)
           for (int n = 0; n < NQ; ++n) acc = fma(dk[n], ftc[n], acc);
         }
         acc = line_dot<T, NQ, LV>(tr + (k * NQ + j) * RS, Di, acc);
-        acc = line_dot<T, NQ, LV>(ts + (k * NQ + i) * RS, Dj, acc);
+        acc = line_dot<T, NQ, LV>(ts + (k * NQ + i) * C::RSS, Dj, acc);
         if (live) re[b * NPT + k * NQ * NQ + col] = fma(jv[kk], acc, rh[kk]);
       }
       }
