@@ -68,9 +68,10 @@ struct ColCfg {
   static constexpr int RS = SC ? (NQ | 1) : S2 ? ((NQ / 2) % 2 ? NQ : NQ + 2) : RSC * VEC;
   // per-direction line strides: RS, except where the bank model of the
   // scalar patterns (tools/col_banks.py) finds a better one for the F_s rows
-  // / F_t columns: fp64 Nq 5 F_s 13, F_t 9 (0.676 -> 0.686 of HBM)
-  static constexpr bool ALT5 = SC && sizeof(T) == 8 && NQ == 5;
-  static constexpr int RSS = ALT5 ? 13 : RS, RST = ALT5 ? 9 : RS;
+  // / F_t columns: fp64 Nq 5 F_s 13, F_t 9 (0.676 -> 0.688 of HBM); fp32
+  // Nq 5 F_s 19, F_t 9
+  static constexpr bool ALT5 = SC && NQ == 5;
+  static constexpr int RSS = ALT5 ? (sizeof(T) == 8 ? 13 : 19) : RS, RST = ALT5 ? 9 : RS;
   static constexpr int TILE = NQ * NQ * RS;            // F_r, one element
   static constexpr int TILES = NQ * NQ * RSS;          // F_s
   static constexpr int TILET = NQ * NQ * RST;          // F_t
