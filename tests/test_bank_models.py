@@ -1,0 +1,54 @@
+"""The shared-memory layout choices of round 2 are the optima of their bank
+models (tools/*_banks.py): the store rotations of the tcgen05 kernel, the
+column kernel's per-direction strides at Nq 5, the lines kernel's line
+strides. CPU only: these pin the models the kernels' comments cite."""
+from __future__ import annotations
+
+import importlib.util
+import pathlib
+
+import pytest
+
+TOOLS = pathlib.Path(__file__).resolve().parents[1] / "tools"
+
+
+def load(name):
+    spec = importlib.util.spec_from_file_location(name, TOOLS / f"{name}.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+# csrc/volume_ltu.cu: gR, gS, gT per Nq
+LTU_GROUPS = {9: ("g2", "g8", "g8"), 10: ("g2", "none", "g8"), 11: ("g4", "none", "g8")}
+
+
+@pytest.mark.parametrize("nq", sorted(LTU_GROUPS))
+def test_ltu_store_rotation_is_the_model_optimum(nq):
+    m = load("ltu_banks")
+    for d, chosen in enumerate(LTU_GROUPS[nq]):
+        costs = {name: m.direction_cost(nq, d, f) for name, f in m.GROUPS.items()}
+        assert costs[chosen] == min(costs.values()), (nq, "RST"[d], costs)
+        assert costs[chosen] <= costs["none"]
+
+
+def test_col_fp64_nq5_strides_are_the_model_optimum():
+    m = load("col_banks")
+    best = {}
+    for key, idx in (("ts", 1), ("tt", 2)):
+        rows = []
+        for rs in range(5, 21):
+            strides = [5, 5, 5]
+            strides[idx] = rs
+            s, l = m.model(5, 5, 8, *strides)
+            rows.append((s[key] + l[key], rs))
+        best[key] = min(rows)
+    # csrc/volume_col.cu ColCfg: F_s 13, F_t 9 at fp64 Nq 5
+    assert best["ts"][1] == 13 and best["tt"][1] == 9
+
+
+def test_lines_nq10_even_stride_beats_the_odd_one():
+    m = load("lines_banks")
+    o10, b10, c10 = m.model(10, 10)
+    o11, b11, c11 = m.model(10, 11)
+    assert o10 + b10 < o11 + b11 and o10 + c10 < o11 + c11
