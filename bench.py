@@ -67,6 +67,7 @@ KERNEL_SOURCES = {
     "lt": ("volume_lt.cu", "lfb_common.cuh", "lfb_math.cuh", "lfb_tma.cuh"),
     "lt32": ("volume_lt32.cu", "lfb_common.cuh", "lfb_tma.cuh"),
     "ltu": ("volume_ltu.cu", "lfb_common.cuh", "lfb_tma.cuh"),
+    "lo": ("volume_lo.cu", "lfb_common.cuh", "lfb_math.cuh", "lfb_tma.cuh"),
     "fused": ("volume_fused.cu", "lfb_common.cuh", "lfb_math.cuh"),
     "basic": ("volume_basic.cu", "lfb_common.cuh"),
 }

@@ -91,8 +91,11 @@ enum {
                                 point owner's registers, S/T through swizzled shared
                                 tiles, per-field q/g stages by bulk copy, software-
                                 pipelined over (element, field) */
-    LFB_VARIANT_LTU = 7      /* fp32 Nq 9..11: the three derivatives as tcgen05 (UMMA)
+    LFB_VARIANT_LTU = 7,     /* fp32 Nq 9..11: the three derivatives as tcgen05 (UMMA)
                                 GEMMs, operands in shared memory, accumulators in TMEM */
+    LFB_VARIANT_LO = 8       /* Nq 9..12: line owners — a thread contracts one R, S and
+                                T line against broadcast D rows, FMA in the storage
+                                precision, point-wise state in shared memory */
 };
 
 LFB_API int lfb_volume_rhs_f64(int Nq, int64_t Ne, double p0, double Rgas, double gam,

@@ -39,9 +39,10 @@ VARIANT_LINES = 4
 VARIANT_COL = 5
 VARIANT_LT = 6
 VARIANT_LTU = 7
+VARIANT_LO = 8
 VARIANTS = {"auto": VARIANT_AUTO, "basic": VARIANT_BASIC, "fused": VARIANT_FUSED,
             "tc": VARIANT_TC, "lines": VARIANT_LINES, "col": VARIANT_COL, "lt": VARIANT_LT,
-            "ltu": VARIANT_LTU}
+            "ltu": VARIANT_LTU, "lo": VARIANT_LO}
 
 MAX_NQ = 16
 

@@ -37,6 +37,11 @@ int volume_lt_f32(int, int64_t, float, float, float, const float *, float *, con
 int volume_ltu_f32(int, int64_t, float, float, float, const float *, float *, const float *,
                    const float *, const float *, cudaStream_t);
 bool ltu_available(int dtype_bytes, int nq);
+int volume_lo_f64(int, int64_t, double, double, double, const double *, double *,
+                  const double *, const double *, const double *, cudaStream_t);
+int volume_lo_f32(int, int64_t, float, float, float, const float *, float *, const float *,
+                  const float *, const float *, cudaStream_t);
+bool lo_available(int dtype_bytes, int nq);
 int volume_col_f64(int, int64_t, double, double, double, const double *, double *,
                    const double *, const double *, const double *, cudaStream_t);
 int volume_col_f32(int, int64_t, float, float, float, const float *, float *, const float *,
@@ -79,6 +84,11 @@ int resolve(int variant, int bytes, int nq) {
     // line tiles (volume_lt*.cu) where they lead: Nq 11, 12 in both
     // precisions, except fp32 Nq 11 where the tcgen05 line GEMMs
     // (volume_ltu.cu) lead (round 2, profiles/r02_sweep_*.jsonl)
+    // line owners (volume_lo.cu, round 2b): fp32 Nq 9, 11 and fp64 Nq 9
+    // (1e8 points: fp32 0.432 -> 0.482, 0.415-0.423 -> 0.464; fp64 0.462 ->
+    // 0.474, profiles/r02b_lo_ab.txt)
+    if ((nq == 9 || (bytes == 4 && nq == 11)) && lfb::lo_available(bytes, nq))
+      return LFB_VARIANT_LO;
     if (nq == 11 && lfb::ltu_available(bytes, nq)) return LFB_VARIANT_LTU;
     if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;
     if (lfb::col_available(bytes, nq)) {
@@ -124,6 +134,9 @@ int lfb_volume_rhs_variant_f64(int variant, int Nq, int64_t Ne, double p0,
     case LFB_VARIANT_LT:
       if (!lfb::lt_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_lt_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LO:
+      if (!lfb::lo_available(8, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lo_f64(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_LTU:
       return LFB_ERR_BAD_VARIANT;
     case LFB_VARIANT_COL:
@@ -162,6 +175,9 @@ int lfb_volume_rhs_variant_f32(int variant, int Nq, int64_t Ne, float p0,
     case LFB_VARIANT_LTU:
       if (!lfb::ltu_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_ltu_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
+    case LFB_VARIANT_LO:
+      if (!lfb::lo_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
+      return lfb::volume_lo_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
     case LFB_VARIANT_COL:
       if (!lfb::col_available(4, Nq)) return LFB_ERR_BAD_VARIANT;
       return lfb::volume_col_f32(Nq, Ne, p0, Rgas, gam, q, rhsq, D, g, Jinv, s);
@@ -203,6 +219,8 @@ int lfb_variant_available(int variant, int dtype_bytes, int Nq) {
       return lfb::lt_available(dtype_bytes, Nq) ? 1 : 0;
     case LFB_VARIANT_LTU:
       return lfb::ltu_available(dtype_bytes, Nq) ? 1 : 0;
+    case LFB_VARIANT_LO:
+      return lfb::lo_available(dtype_bytes, Nq) ? 1 : 0;
     default:
       return 0;
   }
@@ -222,6 +240,7 @@ const char *lfb_variant_name(int variant) {
     case LFB_VARIANT_COL: return "col";
     case LFB_VARIANT_LT: return "lt";
     case LFB_VARIANT_LTU: return "ltu";
+    case LFB_VARIANT_LO: return "lo";
     default: return "unknown";
   }
 }

@@ -29,7 +29,7 @@ SMALL = [(1, 3, 1), (2, 1, 42), (2, 5, 2), (2, 130, 3), (3, 2, 3), (3, 33, 4), (
 
 
 def _variants(nbytes, nq):
-    return [v for v in ("basic", "fused", "tc", "lines", "col", "lt", "ltu")
+    return [v for v in ("basic", "fused", "tc", "lines", "col", "lt", "ltu", "lo")
             if _native.variant_available(v, nbytes, nq)]
 
 
@@ -312,7 +312,8 @@ def test_tc16_fp32_many_elements_against_c_oracle(cuda_device, nq, ne):
 
 @pytest.mark.parametrize("nq,ne", [(9, 701), (10, 650), (11, 613), (12, 597)])
 def test_line_tile_kernels_many_elements_against_c_oracle(cuda_device, nq, ne):
-    """The line-tile kernels (lt fp64 / fp32, ltu fp32 on tcgen05) over more
+    """The line-tile kernels (lt fp64 / fp32, ltu fp32 on tcgen05) and the
+    line-owner kernel (lo) over more
     elements than resident CTAs, so every CTA runs several persistent
     iterations and the stage pipelines wrap across elements; odd Ne puts the
     last element of odd Nq through the column kernel."""
@@ -320,7 +321,7 @@ def test_line_tile_kernels_many_elements_against_c_oracle(cuda_device, nq, ne):
     q, g, j, d = coracle.to_element_batched(st)
     want = coracle.from_element_batched(coracle.volume_f64_eb(nq, q, g, j, d, st.constants))
     for dtype, nbytes, tol in ((torch.float64, 8, TOL64), (torch.float32, 4, TOL32)):
-        for v in [x for x in ("lt", "ltu") if _native.variant_available(x, nbytes, nq)]:
+        for v in [x for x in ("lt", "ltu", "lo") if _native.variant_available(x, nbytes, nq)]:
             ds = DeviceFieldState.from_field_state(st, dtype=dtype)
             volume_rhs_device(ds, variant=v)
             got = ds.rhsq.to(torch.float64).cpu().numpy()

@@ -3,7 +3,7 @@ synccheck, memcheck, initcheck): the B200 counterpart of the reference's
 software race detector hazard_check (lf/interp.py:447-461).
 
 Covers every variant x dtype x Nq family (tc fp64 1-CTA ring / PLANE, tc
-fp32 = TF32 split kernels, line tiles lt fp64 / fp32, ltu (tcgen05), col, lines, fused,
+fp32 = TF32 split kernels, line tiles lt fp64 / fp32, ltu (tcgen05), line owners lo, col, lines, fused,
 basic), the layout and input kernels, the host-buffer pipeline, and one
 emitted reference kernel. Element counts span several elements per CTA so
 the cross-element stage / tile reuse is exercised."""
@@ -28,7 +28,7 @@ CASES = () if ONLY_EMITTED else ((8, 300), (4, 70), (5, 9), (6, 7), (7, 5), (2, 
 for nq, ne in CASES:
     st = make_inputs(BenchmarkConfig(nq=nq, ne=ne, seed=2))
     for dt in (torch.float64, torch.float32):
-        for v in ("tc", "lt", "ltu", "col", "lines", "fused", "basic"):
+        for v in ("tc", "lt", "ltu", "lo", "col", "lines", "fused", "basic"):
             if not _native.variant_available(v, 8 if dt == torch.float64 else 4, nq):
                 continue
             ds = DeviceFieldState.from_field_state(st, dtype=dt)
