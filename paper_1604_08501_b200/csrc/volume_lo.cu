@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
   const int tid = threadIdx.x;
   for (int x = tid; x < NQ * SP; x += NTH) {
     const int o = x / SP, n = x % SP;
-    sD[x] = n < NQ ? D[n * NQ + o] : T(0);  // D[n*NQ + i] = D(i, n)
+    T dv = T(0);
+    if (n < NQ) dv = D[n * NQ + o];  // D[n*NQ + i] = D(i, n); no load past the Nq^2 values
+    sD[x] = dv;
   }
   // own points x = tid + NTH u (A, C): tile positions
   int pR[NPP], pS[NPP], pT[NPP];
