@@ -41,12 +41,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-// one arrival (release, CTA scope: this thread's earlier shared-memory
-// accesses are visible to / complete before the waiters of the phase)
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // global -> shared bulk copy (16-byte aligned addresses, size a multiple of 16)
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {

@@ -345,3 +345,26 @@ def test_padded_column_and_lines_kernels_many_elements(cuda_device, nq, ne):
             got = ds.rhsq.to(torch.float64).cpu().numpy()
             err = max_rel_error(coracle.from_element_batched(got), want)
             assert err <= tol, (v, dtype, err)
+
+
+@pytest.mark.parametrize("nq", [9, 10, 11, 12])
+def test_large_nq_variants_accumulate_dense_D_custom_constants(cuda_device, nq):
+    """Every Nq 9..12 kernel (lines, col, lt, ltu, lo, tc) accumulates into a
+    non-zero rhsq (rhsq += v) with a dense random D (no structure for a
+    transposed or mis-indexed D row to hide behind) and non-default
+    constants, against the oracle."""
+    from paper_1604_08501_b200 import PhysicalConstants
+    c = PhysicalConstants(p0=9.5e4, R=290.0, gamma=1.35)
+    base = make_inputs(BenchmarkConfig(nq=nq, ne=7, seed=nq + 40), constants=c)
+    rng = np.random.default_rng(nq)
+    base.D[...] = rng.uniform(-1.0, 1.0, base.D.shape).astype(base.D.dtype)
+    base.rhsq[...] = rng.uniform(-50.0, 50.0, base.rhsq.shape).astype(base.rhsq.dtype)
+    want = base.rhsq.astype(np.float64) + O.volume_term_f64_batched(base)
+    for dtype, tol in ((np.float64, TOL64), (np.float32, TOL32)):
+        for v in _variants(np.dtype(dtype).itemsize, nq):
+            st = make_inputs(BenchmarkConfig(nq=nq, ne=7, seed=nq + 40), constants=c)
+            st.D[...] = base.D
+            st.rhsq[...] = base.rhsq
+            st = st.astype(dtype)
+            volume_rhs_(st, variant=v)
+            assert max_rel_error(st.rhsq, want) <= tol, (v, dtype)
