@@ -51,6 +51,9 @@
 #ifndef LT_PF  // L2 prefetch of the next element's phase-1 inputs: 0 off,
 #define LT_PF 2  // 1 at element start, 2 in region 6 (two fields ahead)
 #endif
+#ifndef LT_P1S  // phase 1 reads q_1, q_4, g(0, .) from the field / g stages
+#define LT_P1S 1
+#endif
 #ifndef LT_HINT  // L2 policies: phase-1 reads evict_last, stage re-reads evict_first
 #define LT_HINT 0
 #endif
@@ -313,6 +316,15 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
 
     // ---- phase 1: W_d = V_d / rho (V_d = sum_a g(a,d) U_a), p, Jinv ----------
     // every flux is then F_d,b = W_d q_b (+ g(b-1,d) p for b = 1..3); q_0 = rho
+    // (LT_P1S: U_0 = q_1 and Theta = q_4 — the fields at positions 0, 1 —
+    // and g(0, d) — the g stage of position 0 — are read from their stage
+    // copies, 5 of the 14 phase-1 global loads per point)
+    if (LT_P1S) {
+      mbar_wait(&fbar[0], 0u);
+      mbar_wait(&fbar[1], 0u);
+      mbar_wait(&fbar[2], gpar);
+    }
+
     double Wd[3][RPW][KS], pp[RPW][KS], jv[RPW][KS];
 #pragma unroll
     for (int m = 0; m < RPW; ++m) {
@@ -321,10 +333,16 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
       for (int t = 0; t < KS; ++t) {
         const int o = pofs[m] + 4 * t;
         rho[t] = vt[m][t] ? ld1(qe + o) : 1.0;
-        th[t] = vt[m][t] ? __ldg(qe + 4 * NPT + o) : 1.0;
         jv[m][t] = vt[m][t] ? __ldg(jinv + e * NPT + c + o) : 0.0;
+        if (LT_P1S) {
+          th[t] = vt[m][t] ? staged(q + (e * 8 + 4) * NPT, qst + GSLAB, o + c) : 1.0;
+          U[0][t] = vt[m][t] ? staged(q + (e * 8 + 1) * NPT, qst, o + c) : 0.0;
+        } else {
+          th[t] = vt[m][t] ? __ldg(qe + 4 * NPT + o) : 1.0;
+          U[0][t] = vt[m][t] ? ld1(qe + NPT + o) : 0.0;
+        }
 #pragma unroll
-        for (int a = 0; a < 3; ++a) U[a][t] = vt[m][t] ? ld1(qe + (1 + a) * NPT + o) : 0.0;
+        for (int a = 1; a < 3; ++a) U[a][t] = vt[m][t] ? ld1(qe + (1 + a) * NPT + o) : 0.0;
       }
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -333,7 +351,10 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
         for (int t = 0; t < KS; ++t)
 #pragma unroll
           for (int a = 0; a < 3; ++a)
-            gv[a][t] = vt[m][t] ? ld1(ge + (3 * d + a) * NPT + pofs[m] + 4 * t) : 0.0;
+            gv[a][t] = !vt[m][t] ? 0.0
+                       : (LT_P1S && a == 0)
+                           ? staged(g + (e * 9 + 3 * d) * NPT, gst + d * GSLAB, pofs[m] + c + 4 * t)
+                           : ld1(ge + (3 * d + a) * NPT + pofs[m] + 4 * t);
 #pragma unroll
         for (int t = 0; t < KS; ++t)
           Wd[d][m][t] = fma(gv[0][t], U[0][t], fma(gv[1][t], U[1][t], gv[2][t] * U[2][t]));

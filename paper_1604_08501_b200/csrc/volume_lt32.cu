@@ -260,6 +260,18 @@ __global__ void __launch_bounds__(Lt32Cfg<NQ>::THREADS, Lt32Cfg<NQ>::MINB)
     const int64_t en = e + gridDim.x;
 
     // ---- phase 1: W_d = V_d / rho, p, Jinv (FP32) ---------------------------
+    // U_0 = q_1 and Theta = q_4 (the fields at positions 0, 1) and g(0, d)
+    // (the g stage of position 0) come from their stage copies: 5 of the 14
+    // global loads per point (the fp64 kernel's A/B: Nq 12 0.588 -> 0.624)
+    mbar_wait(&bars[0], 0u);
+    mbar_wait(&bars[1], 0u);
+    mbar_wait(&bars[2], gpar);
+    auto sh1 = [](const float *a0) { return (int)((reinterpret_cast<uintptr_t>(a0) & 15) >> 2); };
+    const float *u0s = qst + sh1(q + (e * 8 + 1) * NPT) + c;
+    const float *ths = qst + SLAB + sh1(q + (e * 8 + 4) * NPT) + c;
+    const float *g0s[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) g0s[d] = gst + d * SLAB + sh1(g + (e * 9 + 3 * d) * NPT) + c;
     float Wd[3][2][KS], pp[2][KS], jv[2][KS];
 #pragma unroll
     for (int rho = 0; rho < 2; ++rho) {
@@ -267,12 +279,13 @@ __global__ void __launch_bounds__(Lt32Cfg<NQ>::THREADS, Lt32Cfg<NQ>::MINB)
       for (int t = 0; t < KS; ++t) {
         const int o = pofs[rho] + 4 * t;
         const bool v = vt[rho][t];
-        const float rr = v ? __ldg(qe + o) : 1.f, th = v ? __ldg(qe + 4 * NPT + o) : 1.f;
+        const float rr = v ? __ldg(qe + o) : 1.f, th = v ? ths[o] : 1.f;
         float U[3], gv[9];
+        U[0] = v ? u0s[o] : 0.f;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) U[a] = v ? __ldg(qe + (1 + a) * NPT + o) : 0.f;
+        for (int a = 1; a < 3; ++a) U[a] = v ? __ldg(qe + (1 + a) * NPT + o) : 0.f;
 #pragma unroll
-        for (int x = 0; x < 9; ++x) gv[x] = v ? __ldg(ge + x * NPT + o) : 0.f;
+        for (int x = 0; x < 9; ++x) gv[x] = !v ? 0.f : (x % 3 == 0) ? g0s[x / 3][o] : __ldg(ge + x * NPT + o);
         jv[rho][t] = v ? __ldg(jinv + e * NPT + c + o) : 0.f;
         const float rinv = __frcp_rn(rr);
 #pragma unroll
