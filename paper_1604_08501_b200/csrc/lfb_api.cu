@@ -84,10 +84,11 @@ int resolve(int variant, int bytes, int nq) {
     // line tiles (volume_lt*.cu) where they lead: Nq 11, 12 in both
     // precisions, except fp32 Nq 11 where the tcgen05 line GEMMs
     // (volume_ltu.cu) lead (round 2, profiles/r02_sweep_*.jsonl)
-    // line owners (volume_lo.cu, round 2b): fp32 Nq 9, 11 and fp64 Nq 9
-    // (1e8 points: fp32 0.432 -> 0.482, 0.415-0.423 -> 0.464; fp64 0.462 ->
-    // 0.474, profiles/r02b_lo_ab.txt)
-    if ((nq == 9 || (bytes == 4 && nq == 11)) && lfb::lo_available(bytes, nq))
+    // line owners (volume_lo.cu, round 2b): Nq 9, 10 in both precisions and
+    // fp32 Nq 11 (1e8 points, profiles/r02b_lo_ab.txt, r02b_lo_pf_ab.txt:
+    // fp32 0.43 / 0.48 / 0.42 -> 0.50 / 0.50 / 0.48 over col / col / ltu;
+    // fp64 0.46 / 0.49 -> 0.55 / 0.50 over lines)
+    if ((nq == 9 || nq == 10 || (bytes == 4 && nq == 11)) && lfb::lo_available(bytes, nq))
       return LFB_VARIANT_LO;
     if (nq == 11 && lfb::ltu_available(bytes, nq)) return LFB_VARIANT_LTU;
     if ((nq == 11 || nq == 12) && lfb::lt_available(bytes, nq)) return LFB_VARIANT_LT;

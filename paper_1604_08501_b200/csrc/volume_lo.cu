@@ -36,6 +36,15 @@
 #include "lfb_math.cuh"
 #include "lfb_tma.cuh"
 
+#ifndef LO_PF  // L2 prefetch of the next element's phase-1 inputs at field LO_PF_FIELD
+// (A/B, profiles/r02b_lo_pf_ab.txt: none / field 0 / 4 / 5 / 6 / 7 — 7 leads,
+// fp64 Nq 9 0.47 -> 0.545; also prefetching the next element's q_5..7 and
+// rhsq there was no better)
+#define LO_PF 1
+#endif
+#ifndef LO_PF_FIELD
+#define LO_PF_FIELD 7
+#endif
 #ifndef LO_MINB32  // fp32 CTAs per SM the registers are budgeted for
 #define LO_MINB32 3
 #endif
@@ -179,6 +188,13 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
 
 #pragma unroll 1
     for (int b = 0; b < 8; ++b) {
+      if (LO_PF && b == LO_PF_FIELD && tid == 32 && e + gridDim.x < ne) {
+        // the next element's phase-1 inputs (q_0..4, g, Jinv) into L2
+        const int64_t en = e + gridDim.x;
+        prefetch_l2_range(q + en * 8 * NPT, 5ull * NPT * sizeof(T));
+        prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(T));
+        prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(T));
+      }
       // ---- A (point owners): fluxes -> R, S, T tiles --------------------------
       const bool mom = b >= 1 && b <= 3;
       T rh[NPP];  // rhsq_b, consumed in C

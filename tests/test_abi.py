@@ -86,8 +86,8 @@ def test_error_mapping_raises_reference_style_exceptions():
 # LFB_VARIANT_AUTO per (dtype, Nq): the measured winners of the config-5 sweep
 # (profiles/r02_sweep_*.jsonl, DESIGN.md §4 results table)
 AUTO_F64 = {2: "tc", 3: "col", 4: "tc", 5: "col", 6: "tc", 7: "tc", 8: "tc", 9: "lo",
-            10: "lines", 11: "lt", 12: "lt", 13: "lines"}
-AUTO_F32 = {4: "tc", 5: "col", 6: "tc", 7: "tc", 8: "tc", 9: "lo", 10: "col", 11: "lo",
+            10: "lo", 11: "lt", 12: "lt", 13: "lines"}
+AUTO_F32 = {4: "tc", 5: "col", 6: "tc", 7: "tc", 8: "tc", 9: "lo", 10: "lo", 11: "lo",
             12: "lt", 13: "tc", 16: "tc"}
 
 
