@@ -51,6 +51,11 @@
 #ifndef LT_PF  // L2 prefetch of the next element's phase-1 inputs: 0 off,
 #define LT_PF 2  // 1 at element start, 2 in region 6 (two fields ahead)
 #endif
+#ifndef LT_PF_REGION  // LT_PF = 2: the region whose end issues the prefetch
+// (A/B after the stage-fed phase 1, profiles/r02b_lt_pf_ab.txt: regions 1..7
+// -> 3 leads, Nq 12 / 11 0.623 / 0.496 at 6 -> 0.674 / 0.512)
+#define LT_PF_REGION 3
+#endif
 #ifndef LT_P1S  // phase 1 reads q_1, q_4, g(0, .) from the field / g stages
 #define LT_P1S 1
 #endif
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(LtCfg<NQ, RPW>::THREADS, LtCfg<NQ, RPW>::MINB)
       for (int m = 0; m < RPW; ++m)
 #pragma unroll
         for (int t = 0; t < KS; ++t) part[f & 1][m][t] = pnew[m][t];
-      if (LT_PF == 2 && f == 6 && tid == 32 && en < ne) {
+      if (LT_PF == 2 && f == LT_PF_REGION && tid == 32 && en < ne) {
         prefetch_l2_range(q + en * 8 * NPT, 5ull * NPT * sizeof(double));
         prefetch_l2_range(g + en * 9 * NPT, 9ull * NPT * sizeof(double));
         prefetch_l2_range(jinv + en * NPT, 1ull * NPT * sizeof(double));
