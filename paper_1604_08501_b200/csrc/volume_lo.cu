@@ -4,31 +4,28 @@
 // bound by its shared-memory pipe — every point re-reads the three Nq-long
 // flux lines it contracts, ~3 Nq values per point and field — and the
 // tensor-core line kernels (volume_lt*.cu, volume_ltu.cu) by the register
-// footprint of one 1000-1700 point element per SM. Here a thread owns LINES,
-// not points, so D(o, .) is the only operand that changes along a
-// contraction and is read as a warp-wide broadcast:
+// footprint of one 1000-1700 point element per SM. Here the contractions are
+// done by LINE owners, so D(o, .) is the only operand that changes along a
+// contraction and is read as a warp-wide broadcast; fluxes and write-back
+// are done by POINT owners, so every global access is coalesced.
 //
-//   thread te = a + Nq b of an element owns R-line (j=a, k=b), S-line
-//   (i=a, k=b) and T-line (i=a, j=b);
-//   phase 1 (per element): for the points of its R-line (contiguous in
-//     memory) W_d = V_d / rho (V_d = sum_a g(a,d) U_a), p and Jinv go to
-//     shared state rows (one 16-byte aligned row per thread);
+//   CTA = one element, ceil(Nq^2 / 32) warps, several CTAs per SM;
+//   point owners: x = tid + THREADS u; line owner te < Nq^2 owns R-line
+//     (j, k), S-line (i, k) and T-line (i, j) with (te % Nq, te / Nq);
+//   phase 1 (per element, point owners): W_d = V_d / rho (V_d = sum_a
+//     g(a,d) U_a) and p -> shared state rows by point;
 //   per field b:
-//     A  fluxes at the R-line points: F_r stays in registers, F_s and F_t
-//        go to the S and T tiles (rows = lines);                  | barrier
-//     B  the thread loads its S-line and T-line rows, then for every output
-//        index o reads D(o, .) (broadcast 16-byte loads) and forms the
-//        three dot products: R(o) in registers, S(o) and T(o) written back
-//        over its own rows;                                       | barrier
-//     C  rhsq_b += Jinv (R + S + T) along the R-line (S and T read at the
-//        flux-store positions).                                   | barrier
-//   Shared traffic per point and field: 2 flux stores, 2 line reads, 2
-//   output stores, 2 combine reads and ~NQ/VEC broadcast D reads per output
-//   row — a few wavefronts per point instead of the column kernel's ~3 Nq
-//   values. Tile row strides from the bank model tools/lo_banks.py.
-// HBM traffic is the 34 values/pt minimum (q, g, Jinv read once; the
-// per-field re-reads of q_b and g(b-1, .) hit L2; rhsq read and written
-// once). Several CTAs (elements) per SM hide the three barriers per field.
+//     A  point owners: F_r, F_s, F_t -> the R / S / T tiles (rows = lines);
+//        q of the next field and rhsq_b go to registers          | barrier
+//     B  line owners: load the three rows, then per output index o one
+//        broadcast D(o, .) row against three dot products, the outputs
+//        written over the own rows                                | barrier
+//     C  point owners: rhsq_b += Jinv (R + S + T)                 | barrier
+//   the next element's phase-1 slabs are L2-prefetched at field 7.
+// Shared traffic per point and field is ~0.5 wavefronts (12 scalar accesses
+// + the state reads + one broadcast per output row); tile row strides from
+// the bank model tools/lo_banks.py. HBM traffic is the 34 values/pt minimum
+// (q, g, Jinv read once from HBM; the per-field re-reads hit L2).
 
 #include <stdint.h>
 
@@ -84,12 +81,17 @@ struct LoCfg {
   static constexpr int SP = ((CH0 % 2) ? CH0 : CH0 + 1) * VEC;  // D row stride
   static constexpr int RSR = lo_rsr(NQ, sizeof(T));
   static constexpr int RSS = lo_rss(NQ, sizeof(T)), RST = lo_rst(NQ, sizeof(T));
-  // state [5][NPT] (W_r, W_s, W_t, p, Jinv by point), R / S / T tiles
+  // state [4][NPT] (W_r, W_s, W_t, p by point; Jinv is read from global at
+  // the write-back — a fifth row cost CTAs per SM, profiles/r02b_lo_jg_ab.txt),
+  // R / S / T tiles
   // [TPE][RS*], D rows [NQ][SP] (row o = D(o, .))
   static constexpr int ST = (NPT + VEC - 1) / VEC * VEC;
-  static constexpr int DOFF = (5 * ST + TPE * (RSR + RSS + RST) + VEC - 1) / VEC * VEC;
+  static constexpr int NSR = 4;  // state rows
+  static constexpr int DOFF = (NSR * ST + TPE * (RSR + RSS + RST) + VEC - 1) / VEC * VEC;
   static constexpr size_t SMEM = sizeof(T) * ((size_t)DOFF + NQ * SP);
-  static constexpr int MINB = sizeof(T) == 4 ? LO_MINB32 : 2;
+  // fp64: 3 CTAs' registers at Nq <= 10 (fp64 Nq 10 0.495 -> 0.511; at
+  // Nq 11, 12 the 168-register cap spills, 0.48 -> 0.43)
+  static constexpr int MINB = sizeof(T) == 4 ? LO_MINB32 : (NQ <= 10 ? 3 : 2);
 };
 
 template <typename T>
@@ -125,8 +127,8 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
   constexpr int NTH = C::THREADS;
   using V = typename LoVec<T>::type;
   extern __shared__ __align__(16) unsigned char lo_raw[];
-  T *const sst = reinterpret_cast<T *>(lo_raw);  // state [5][ST]
-  T *const sR = sst + 5 * ST;                     // R tile [TPE][RSR]: row (k,j), pos i
+  T *const sst = reinterpret_cast<T *>(lo_raw);  // state [4][ST]
+  T *const sR = sst + C::NSR * ST;                    // R tile [TPE][RSR]: row (k,j), pos i
   T *const sS = sR + TPE * RSR;                   // S tile [TPE][RSS]: row (k,i), pos j
   T *const sT = sS + TPE * RSS;                   // T tile [TPE][RST]: row (j,i), pos k
   T *const sD = sst + C::DOFF;                    // D rows [NQ][SP] (16-byte aligned)
@@ -179,7 +181,6 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
         for (int d = 0; d < 3; ++d)
           sst[d * ST + tid + o] = fma(gv[3 * d], U[0], fma(gv[3 * d + 1], U[1], gv[3 * d + 2] * U[2])) * rinv;
         sst[3 * ST + tid + o] = p;
-        sst[4 * ST + tid + o] = __ldg(je + o);
       }
     }
     T qv[NPP];  // q_b at the own points, loaded a field ahead
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
       for (int u = 0; u < NPP; ++u) {
         if (own(u)) {
           const int o = NTH * u;
-          re[b * NPT + o] = fma(sst[4 * ST + tid + o], sR[pR[u]] + sS[pS[u]] + sT[pT[u]], rh[u]);
+          re[b * NPT + o] = fma(__ldg(je + o), sR[pR[u]] + sS[pS[u]] + sT[pT[u]], rh[u]);
         }
       }
       __syncthreads();
