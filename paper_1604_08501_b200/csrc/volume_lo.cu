@@ -42,6 +42,12 @@
 #ifndef LO_PF_FIELD
 #define LO_PF_FIELD 7
 #endif
+#ifndef LO_CS  // streaming cache operator on last-use loads and the rhsq stores
+#define LO_CS 1
+#endif
+#ifndef LO_RPF  // rhsq into L2: 0 the element's 8 slabs at its start, 1 a field
+#define LO_RPF 2  // ahead, 2 a field ahead for fp64 only (profiles/r02b_lo_l2_ab.txt)
+#endif
 #ifndef LO_MINB32  // fp32 CTAs per SM the registers are budgeted for
 #define LO_MINB32 3
 #endif
@@ -105,6 +111,17 @@ struct LoVec<double> {
   using type = double2;
 };
 
+// last-use loads / write-once stores with the streaming (evict-first) cache
+// operator, so an element's dead lines leave L2 before the live ones
+template <typename T>
+__device__ __forceinline__ T lo_ld_last(const T *p) {
+  return LO_CS ? __ldcs(p) : __ldg(p);
+}
+template <typename T>
+__device__ __forceinline__ void lo_st_once(T *p, T v) {
+  if (LO_CS) __stcs(p, v); else *p = v;
+}
+
 template <typename T>
 __device__ __forceinline__ void lo_scalars(T rho, T th, T p0, T Rp0, T gam, T &rinv, T &p) {
   if constexpr (sizeof(T) == 4) {
@@ -125,6 +142,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
   constexpr int NPT = C::NPT, TPE = C::TPE, SP = C::SP, ST = C::ST, NPP = C::NPP;
   constexpr int RSR = C::RSR, RSS = C::RSS, RST = C::RST, VEC = C::VEC, OUN = LO_OUNROLL;
   constexpr int NTH = C::THREADS;
+  constexpr bool RPF = LO_RPF == 1 || (LO_RPF == 2 && sizeof(T) == 8);
   using V = typename LoVec<T>::type;
   extern __shared__ __align__(16) unsigned char lo_raw[];
   T *const sst = reinterpret_cast<T *>(lo_raw);  // state [4][ST]
@@ -162,7 +180,8 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
     T *re = rhsq + e * 8 * NPT + tid;
     if (tid == 0) {  // the slabs first touched in the field loop
       prefetch_l2_range(q + e * 8 * NPT + 5 * NPT, 3ull * NPT * sizeof(T));
-      prefetch_l2_range(rhsq + e * 8 * NPT, 8ull * NPT * sizeof(T));
+      if (!RPF) prefetch_l2_range(rhsq + e * 8 * NPT, 8ull * NPT * sizeof(T));
+      else prefetch_l2_range(rhsq + e * 8 * NPT, 1ull * NPT * sizeof(T));
     }
     // ---- phase 1 (point owners): W_d, p -> state ----------------------------
 #pragma unroll
@@ -200,7 +219,8 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
       const bool mom = b >= 1 && b <= 3;
       T rh[NPP];  // rhsq_b, consumed in C
 #pragma unroll
-      for (int u = 0; u < NPP; ++u) rh[u] = own(u) ? re[b * NPT + NTH * u] : T(0);
+      for (int u = 0; u < NPP; ++u) rh[u] = own(u) ? lo_ld_last(re + b * NPT + NTH * u) : T(0);
+      if (RPF && tid == 0 && b < 7) prefetch_l2_range(rhsq + (e * 8 + b + 1) * NPT, 1ull * NPT * sizeof(T));
 #pragma unroll
       for (int u = 0; u < NPP; ++u) {
         if (own(u)) {
@@ -211,7 +231,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
           if (mom) {
             const T pv = sst[3 * ST + tid + o];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) f[d] = fma(__ldg(ge + (3 * d + b - 1) * NPT + o), pv, f[d]);
+            for (int d = 0; d < 3; ++d) f[d] = fma(lo_ld_last(ge + (3 * d + b - 1) * NPT + o), pv, f[d]);
           }
           sR[pR[u]] = f[0];
           sS[pS[u]] = f[1];
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
       }
       if (b < 7) {
 #pragma unroll
-        for (int u = 0; u < NPP; ++u) qv[u] = own(u) ? __ldg(qe + (b + 1) * NPT + NTH * u) : T(0);
+        for (int u = 0; u < NPP; ++u) qv[u] = own(u) ? lo_ld_last(qe + (b + 1) * NPT + NTH * u) : T(0);
       }
       __syncthreads();
       // ---- B (line owners): contractions, outputs over the own rows ----------
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
       for (int u = 0; u < NPP; ++u) {
         if (own(u)) {
           const int o = NTH * u;
-          re[b * NPT + o] = fma(__ldg(je + o), sR[pR[u]] + sS[pS[u]] + sT[pT[u]], rh[u]);
+          lo_st_once(re + b * NPT + o, fma(__ldg(je + o), sR[pR[u]] + sS[pS[u]] + sT[pT[u]], rh[u]));
         }
       }
       __syncthreads();
