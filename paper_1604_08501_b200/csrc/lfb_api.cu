@@ -87,7 +87,7 @@ int resolve(int variant, int bytes, int nq) {
     // line owners (volume_lo.cu, round 2b): Nq 9, 10 in both precisions and
     // fp32 Nq 11 (1e8 points, profiles/r02b_lo_ab.txt, r02b_lo_pf_ab.txt:
     // fp32 0.43 / 0.48 / 0.42 -> 0.50 / 0.50 / 0.48 over col / col / ltu;
-    // fp64 0.46 / 0.49 -> 0.55 / 0.50 over lines)
+    // fp64 0.46 / 0.48 -> 0.58 / 0.53 over lines, profiles/r02b_lo_l2_ab.txt)
     if ((nq == 9 || nq == 10 || (bytes == 4 && nq == 11)) && lfb::lo_available(bytes, nq))
       return LFB_VARIANT_LO;
     if (nq == 11 && lfb::ltu_available(bytes, nq)) return LFB_VARIANT_LTU;
