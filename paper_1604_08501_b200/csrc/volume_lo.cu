@@ -51,9 +51,6 @@
 #ifndef LO_MINB32  // fp32 CTAs per SM the registers are budgeted for
 #define LO_MINB32 3
 #endif
-#ifndef LO_NB  // flux tile buffers (2: one barrier less per field)
-#define LO_NB 2
-#endif
 #ifndef LO_OUNROLL  // unroll of the output-row loop of the line contractions
 #define LO_OUNROLL 2
 #endif
@@ -89,8 +86,7 @@ struct LoCfg {
   static constexpr int RSS = lo_rss(NQ, sizeof(T)), RST = lo_rst(NQ, sizeof(T));
   // state [4][NPT] (W_r, W_s, W_t, p by point; Jinv is read from global at
   // the write-back — a fifth row cost CTAs per SM, profiles/r02b_lo_jg_ab.txt),
-  // R / S / T tiles
-  // [TPE][RS*], D rows [NQ][SP] (row o = D(o, .))
+  // R / S / T tiles [TPE][RS*], D rows [NQ][SP] (row o = D(o, .))
   static constexpr int ST = (NPT + VEC - 1) / VEC * VEC;
   static constexpr int NSR = 4;  // state rows
   static constexpr int DOFF = (NSR * ST + TPE * (RSR + RSS + RST) + VEC - 1) / VEC * VEC;
@@ -146,7 +142,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
   using V = typename LoVec<T>::type;
   extern __shared__ __align__(16) unsigned char lo_raw[];
   T *const sst = reinterpret_cast<T *>(lo_raw);  // state [4][ST]
-  T *const sR = sst + C::NSR * ST;                    // R tile [TPE][RSR]: row (k,j), pos i
+  T *const sR = sst + C::NSR * ST;                // R tile [TPE][RSR]: row (k,j), pos i
   T *const sS = sR + TPE * RSR;                   // S tile [TPE][RSS]: row (k,i), pos j
   T *const sT = sS + TPE * RSS;                   // T tile [TPE][RST]: row (j,i), pos k
   T *const sD = sst + C::DOFF;                    // D rows [NQ][SP] (16-byte aligned)
