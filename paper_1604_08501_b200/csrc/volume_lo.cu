@@ -51,8 +51,9 @@
 #ifndef LO_MINB32  // fp32 CTAs per SM the registers are budgeted for
 #define LO_MINB32 3
 #endif
-#ifndef LO_OUNROLL  // unroll of the output-row loop of the line contractions
-#define LO_OUNROLL 2
+#ifndef LO_OUNROLL  // unroll of the output-row loop of the line contractions (0: full;
+// profiles/r02b_lo_unroll_ab.txt: 1 / 2 / 3 / 6 / 9 / full, full +1-4 %)
+#define LO_OUNROLL 0
 #endif
 
 namespace lfb {
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(LoCfg<T, NQ>::THREADS, LoCfg<T, NQ>::MINB)
                      const T *__restrict__ jinv) {
   using C = LoCfg<T, NQ>;
   constexpr int NPT = C::NPT, TPE = C::TPE, SP = C::SP, ST = C::ST, NPP = C::NPP;
-  constexpr int RSR = C::RSR, RSS = C::RSS, RST = C::RST, VEC = C::VEC, OUN = LO_OUNROLL;
+  constexpr int RSR = C::RSR, RSS = C::RSS, RST = C::RST, VEC = C::VEC, OUN = LO_OUNROLL ? LO_OUNROLL : NQ;
   constexpr int NTH = C::THREADS;
   constexpr bool RPF = LO_RPF == 1 || (LO_RPF == 2 && sizeof(T) == 8);
   using V = typename LoVec<T>::type;
