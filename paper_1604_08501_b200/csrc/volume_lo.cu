@@ -62,11 +62,12 @@ namespace {
 
 // tile row strides (values) from the bank model tools/lo_banks.py, per
 // (dtype bytes, Nq 9..12): point-owner and line-owner accesses of each tile
-// (fp32 Nq 11 keeps S at 11: the model's 35 triples the tile and measured
-// 0.464 -> 0.448 of HBM, fewer CTAs per SM)
+// (fp32 Nq 11: S at 15, the model's runner-up at a third of the tile size of
+// its optimum 35 — measured 0.485 / 0.513 / 0.506 / 0.498 at S = 11 / 15 /
+// 27 / 35, profiles/r02b_lo_strides_ab.txt)
 constexpr int lo_rsr(int nq, int bytes) { return nq == 12 ? 13 : nq; }
 constexpr int lo_rss(int nq, int bytes) {
-  return bytes == 4 ? (nq == 9 ? 25 : nq == 10 ? 17 : nq == 11 ? 11 : 15)
+  return bytes == 4 ? (nq == 9 ? 25 : nq == 10 ? 17 : nq == 11 ? 15 : 15)
                     : (nq == 9 ? 9 : nq == 10 ? 13 : nq == 11 ? 19 : 13);
 }
 constexpr int lo_rst(int nq, int bytes) {

@@ -55,11 +55,11 @@ def test_lines_nq10_even_stride_beats_the_odd_one():
 
 
 # csrc/volume_lo.cu lo_rsr / lo_rss / lo_rst: (dtype bytes, Nq) -> R, S, T row strides
-LO_STRIDES = {(4, 9): (9, 25, 17), (4, 10): (10, 17, 11), (4, 11): (11, 11, 11),
+LO_STRIDES = {(4, 9): (9, 25, 17), (4, 10): (10, 17, 11), (4, 11): (11, 15, 11),
               (4, 12): (13, 15, 13), (8, 9): (9, 9, 17), (8, 10): (10, 13, 11),
               (8, 11): (11, 19, 25), (8, 12): (13, 13, 13)}
-# measured exception: fp32 Nq 11 keeps S at 11 (the model's 35 triples the
-# tile: fewer CTAs per SM, 0.464 -> 0.448 of HBM)
+# measured exception: fp32 Nq 11 takes S = 15 (modelled 254 wavefronts vs the
+# optimum's 192 at 35, a third of the tile; measured 0.513 vs 0.498 of HBM)
 LO_MEASURED = {(4, 11, "S")}
 
 
@@ -70,5 +70,8 @@ def test_lo_strides_are_the_model_optimum(nbytes, nq):
     for kind, rs in zip("RST", LO_STRIDES[(nbytes, nq)]):
         costs = {r: m.cost(nq, nbytes, r, kind, threads) for r in range(nq, nq + 25)}
         if (nbytes, nq, kind) in LO_MEASURED:
+            # within a third of the optimum and the best stride no wider than 15
+            small = {r: c for r, c in costs.items() if r <= 15}
+            assert costs[rs] == min(small.values()), (nbytes, nq, kind, rs)
             continue
         assert costs[rs] == min(costs.values()), (nbytes, nq, kind, rs, min(costs, key=costs.get))
